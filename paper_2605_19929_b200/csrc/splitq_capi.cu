@@ -1,0 +1,710 @@
+// C-ABI implementation (include/splitq.h): layer packing, workspace layout and
+// the launch sequence of the split-linear forward on one CUDA stream:
+//   compact_text_rows -> K1 quantize -> LR1 (CWS) -> LR1 (MAC) -> split GEMM
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/splitq.h"
+#include "gemm_sm100.cuh"
+#include "quantize.cuh"
+#include "tma_host.cuh"
+
+using namespace splitq;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      return fail(SPLITQ_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));     \
+  } while (0)
+
+inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+int sm_count(int device) {
+  static int cache[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (!cache[device]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0)
+      v = 148;
+    cache[device] = v;
+  }
+  return cache[device];
+}
+
+// QuantSpec -> device spec (quantizer.py:41-51). Codes are stored centred
+// (q - zp) as s8 whenever that fits (symmetric, or asymmetric <= 7 bits),
+// otherwise as u8 with the zero point applied in the GEMM epilogue.
+int make_spec(splitq_qspec_t s, QSpecDev* out, const char* what) {
+  if (s.bits < 2 || s.bits > 8)
+    return fail(SPLITQ_ERR_UNSUPPORTED,
+                "%s: the GPU path supports integer bit widths 2..8 (got %d); identity and "
+                ">8-bit specs stay on the CPU reference",
+                what, s.bits);
+  if (s.symmetric) {
+    out->qmin = -(1 << (s.bits - 1)) + 1;
+    out->qmax = (1 << (s.bits - 1)) - 1;
+    out->sym = 1;
+    out->centered = 1;
+  } else {
+    out->qmin = 0;
+    out->qmax = (1 << s.bits) - 1;
+    out->sym = 0;
+    out->centered = s.bits <= 7 ? 1 : 0;
+  }
+  return SPLITQ_OK;
+}
+
+splitq_qspec_t with_floor(splitq_qspec_t s, int floor_bits) {  // quantizer.py:53-57
+  if (s.bits < floor_bits) s.bits = floor_bits;
+  return s;
+}
+
+struct DevBuf {
+  std::vector<void*> ptrs;
+  int alloc(void** out, size_t bytes) {
+    *out = nullptr;
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(out, bytes);
+    if (e != cudaSuccess) return fail(SPLITQ_ERR_CUDA, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+    ptrs.push_back(*out);
+    return SPLITQ_OK;
+  }
+  template <typename T>
+  int upload(T** out, const T* host, size_t count) {
+    int rc = alloc(reinterpret_cast<void**>(out), count * sizeof(T));
+    if (rc) return rc;
+    if (count) {
+      cudaError_t e = cudaMemcpy(*out, host, count * sizeof(T), cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return fail(SPLITQ_ERR_CUDA, "cudaMemcpy: %s", cudaGetErrorString(e));
+    }
+    return SPLITQ_OK;
+  }
+  void release() {
+    for (void* p : ptrs) cudaFree(p);
+    ptrs.clear();
+  }
+};
+
+// K x N row-major centred codes -> N x ld K-major (zero padded) + column sums.
+void transpose_codes(const int8_t* q, int64_t K, int64_t N, int64_t ld, std::vector<int8_t>& out,
+                     std::vector<int32_t>& colsum) {
+  out.assign((size_t)N * ld, 0);
+  colsum.assign((size_t)N, 0);
+  for (int64_t k = 0; k < K; ++k) {
+    const int8_t* src = q + k * N;
+    for (int64_t n = 0; n < N; ++n) {
+      out[(size_t)n * ld + k] = src[n];
+      colsum[n] += src[n];
+    }
+  }
+}
+
+double pow2_ceil(double v) {  // smallest power of two >= v (v > 0)
+  int e;
+  const double m = std::frexp(v, &e);  // v = m * 2^e, m in [0.5, 1)
+  return m == 0.5 ? std::ldexp(1.0, e - 1) : std::ldexp(1.0, e);
+}
+
+}  // namespace
+
+struct splitq_layer_s {
+  int device = 0;
+  int64_t d_in = 0, d_out = 0, n_main = 0, n_text = 0, n_vis = 0, r_s = 0, r_c = 0;
+  QSpecDev act{}, aux{};
+  int use_cws = 0, use_mac = 0;
+  int64_t ld_main = 0, ld_text = 0, ld_vis = 0;
+  int64_t r_s16 = 0, r_c16 = 0, k_lr = 0;
+  DevBuf mem;
+  int* c_main = nullptr; double* d_main = nullptr;
+  int* c_text = nullptr; double* d_text = nullptr;
+  int* c_vis = nullptr; double* d_vis = nullptr;
+  int8_t* b_main = nullptr; float* s_main = nullptr; int* cs_main = nullptr;
+  int8_t* b_text = nullptr; float* s_text = nullptr; int* cs_text = nullptr;
+  int8_t* b_vis = nullptr; float* s_vis = nullptr; int* cs_vis = nullptr;
+  int8_t* b_us = nullptr; float* s_us = nullptr; int* cs_us = nullptr;
+  int8_t* b_uc = nullptr; float* s_uc = nullptr; int* cs_uc = nullptr;
+  __half* b_lr = nullptr; float* kappa = nullptr;
+};
+
+namespace {
+
+int pack_weight(splitq_layer_s* L, const int8_t* q, const double* s, int64_t K, int64_t N,
+                int64_t ld, int8_t** b, float** sc, int** cs, double extra_div = 1.0,
+                const std::vector<double>* per_col_div = nullptr) {
+  std::vector<int8_t> t;
+  std::vector<int32_t> colsum;
+  transpose_codes(q, K, N, ld, t, colsum);
+  std::vector<float> sf((size_t)N);
+  for (int64_t n = 0; n < N; ++n) {
+    double v = s[n] / extra_div;
+    if (per_col_div) v /= (*per_col_div)[n];
+    sf[n] = (float)v;
+  }
+  int rc = L->mem.upload(b, t.data(), t.size());
+  if (!rc) rc = L->mem.upload(sc, sf.data(), sf.size());
+  if (!rc) rc = L->mem.upload(cs, colsum.data(), colsum.size());
+  return rc;
+}
+
+int validate_index_set(const int64_t* c, int64_t n, int64_t dim, const char* name) {
+  for (int64_t i = 0; i < n; ++i) {
+    if (c[i] < 0 || c[i] >= dim) return fail(SPLITQ_ERR_INVALID, "%s index out of range", name);
+    if (i && c[i] <= c[i - 1]) return fail(SPLITQ_ERR_INVALID, "%s must be strictly ascending", name);
+  }
+  return SPLITQ_OK;
+}
+
+int check_codes(const int8_t* q, int64_t count, const QSpecDev& s, const char* name) {
+  // centred weight codes lie in [qmin - zp, qmax - zp] subset of [-(qmax-qmin), qmax-qmin]
+  const int lim = s.qmax - s.qmin;
+  for (int64_t i = 0; i < count; ++i)
+    if (q[i] < -lim || q[i] > lim) return fail(SPLITQ_ERR_INVALID, "%s code out of range", name);
+  return SPLITQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* splitq_last_error(void) { return g_last_error.c_str(); }
+int splitq_version(void) { return 1; }
+
+int splitq_device_sm_count(int device, int* out) {
+  if (!out) return fail(SPLITQ_ERR_INVALID, "null output");
+  *out = sm_count(device);
+  return SPLITQ_OK;
+}
+
+int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t* out) {
+  if (!d || !out) return fail(SPLITQ_ERR_INVALID, "null argument");
+  *out = nullptr;
+  if (d->d_in <= 0 || d->d_out <= 0) return fail(SPLITQ_ERR_INVALID, "empty layer");
+  if (d->n_main + d->n_text + d->n_vision != d->d_in)
+    return fail(SPLITQ_ERR_INVALID, "channel sets must cover exactly 0..dim-1");
+  if (d->n_main < d->n_text || d->n_main < d->n_vision)
+    return fail(SPLITQ_ERR_INVALID, "main set must be at least as large as each outlier set");
+  QSpecDev act, wsp, aux, waux;
+  int rc = make_spec(d->act, &act, "act_spec");
+  if (!rc) rc = make_spec(d->weight, &wsp, "weight_spec");
+  if (rc) return rc;
+  const int floor_bits = d->aux_bits_floor;
+  rc = make_spec(with_floor(d->act, floor_bits), &aux, "act_spec (aux floor)");
+  if (!rc) rc = make_spec(with_floor(d->weight, floor_bits), &waux, "weight_spec (aux floor)");
+  if (rc) return rc;
+  if (wsp.qmax - wsp.qmin > 127 || waux.qmax - waux.qmin > 127)
+    return fail(SPLITQ_ERR_UNSUPPORTED, "weight codes must fit int8 (asymmetric 8-bit weights unsupported)");
+  if (d->use_cws && (d->r_cws <= 0 || d->r_cws > std::min(d->n_main, d->d_out)))
+    return fail(SPLITQ_ERR_INVALID, "branch rank exceeds min(path width, d_out)");
+  if (d->use_mac && (d->r_mac <= 0 || d->r_mac > std::min(d->n_main, d->d_out)))
+    return fail(SPLITQ_ERR_INVALID, "branch rank exceeds min(path width, d_out)");
+  if ((rc = validate_index_set(d->c_main, d->n_main, d->d_in, "c_main"))) return rc;
+  if ((rc = validate_index_set(d->c_text, d->n_text, d->d_in, "c_text"))) return rc;
+  if ((rc = validate_index_set(d->c_vision, d->n_vision, d->d_in, "c_vision"))) return rc;
+  {
+    std::vector<char> seen((size_t)d->d_in, 0);
+    for (auto [c, n] : {std::pair<const int64_t*, int64_t>{d->c_main, d->n_main},
+                        {d->c_text, d->n_text}, {d->c_vision, d->n_vision}})
+      for (int64_t i = 0; i < n; ++i) {
+        if (seen[c[i]]) return fail(SPLITQ_ERR_INVALID, "channel sets must be pairwise disjoint");
+        seen[c[i]] = 1;
+      }
+  }
+  if ((rc = check_codes(d->q_main, d->n_main * d->d_out, wsp, "q_main"))) return rc;
+  if (d->n_text && (rc = check_codes(d->q_text, d->n_text * d->d_out, waux, "q_text"))) return rc;
+  if (d->n_vision && (rc = check_codes(d->q_vision, d->n_vision * d->d_out, waux, "q_vision")))
+    return rc;
+
+  CUDA_TRY(cudaSetDevice(device));
+  auto* L = new splitq_layer_s();
+  L->device = device;
+  L->d_in = d->d_in;
+  L->d_out = d->d_out;
+  L->n_main = d->n_main;
+  L->n_text = d->n_text;
+  L->n_vis = d->n_vision;
+  L->act = act;
+  L->aux = aux;
+  L->use_cws = d->use_cws ? 1 : 0;
+  L->use_mac = d->use_mac ? 1 : 0;
+  L->r_s = L->use_cws ? d->r_cws : 0;
+  L->r_c = L->use_mac ? d->r_mac : 0;
+  L->ld_main = round_up(L->n_main, 16);
+  L->ld_text = round_up(std::max<int64_t>(L->n_text, 1), 16);
+  L->ld_vis = round_up(std::max<int64_t>(L->n_vis, 1), 16);
+  L->r_s16 = round_up(L->r_s, 16);
+  L->r_c16 = round_up(L->r_c, 16);
+  L->k_lr = (L->r_s + L->r_c) ? round_up(L->r_s16 + L->r_c16, 64) : 0;
+
+  auto cleanup = [&](int code) {
+    L->mem.release();
+    delete L;
+    return code;
+  };
+  auto to_i32 = [](const int64_t* c, int64_t n) {
+    std::vector<int32_t> v((size_t)n);
+    for (int64_t i = 0; i < n; ++i) v[i] = (int32_t)c[i];
+    return v;
+  };
+  {
+    auto cm = to_i32(d->c_main, d->n_main), ct = to_i32(d->c_text, d->n_text),
+         cv = to_i32(d->c_vision, d->n_vision);
+    if ((rc = L->mem.upload(&L->c_main, cm.data(), cm.size()))) return cleanup(rc);
+    if ((rc = L->mem.upload(&L->c_text, ct.data(), ct.size()))) return cleanup(rc);
+    if ((rc = L->mem.upload(&L->c_vis, cv.data(), cv.size()))) return cleanup(rc);
+    if ((rc = L->mem.upload(&L->d_main, d->scale_main, d->n_main))) return cleanup(rc);
+    if ((rc = L->mem.upload(&L->d_text, d->scale_text, d->n_text))) return cleanup(rc);
+    if ((rc = L->mem.upload(&L->d_vis, d->scale_vision, d->n_vision))) return cleanup(rc);
+  }
+  const int64_t N = d->d_out;
+  if ((rc = pack_weight(L, d->q_main, d->s_main, d->n_main, N, L->ld_main, &L->b_main, &L->s_main,
+                        &L->cs_main)))
+    return cleanup(rc);
+  if (L->n_text && (rc = pack_weight(L, d->q_text, d->s_text, d->n_text, N, L->ld_text, &L->b_text,
+                                     &L->s_text, &L->cs_text)))
+    return cleanup(rc);
+  if (L->n_vis && (rc = pack_weight(L, d->q_vision, d->s_vision, d->n_vision, N, L->ld_vis,
+                                    &L->b_vis, &L->s_vis, &L->cs_vis)))
+    return cleanup(rc);
+
+  if (L->k_lr) {
+    // Low-rank first stage: A_lr[i, c] = (S_a[i] / rho_i) * (S_u[c] / sigma_c) * acc[i, c]
+    // with sigma_c a power of two bounding |A_lr| by 2^15 (fp16-safe for any input).
+    // Second stage B_lr (fp16, d_out x k_lr, K-major):
+    //   CWS  cols [0, r_s):          qv_s[c, j] * sigma_c / kappa_j          (exact)
+    //   MAC  cols [r_s16, r_s16+r_c): qv_c[c, j] * (S_vc[j]/colf[j]) * sigma'_c / kappa_j
+    // and the epilogue adds rho_i * (kappa_j * colf[j]) * f[i, j], colf = S_vs (or S_vc).
+    const int64_t K = d->n_main;
+    auto sigmas = [&](const int8_t* qu, const double* su, int64_t r, const QSpecDev& a) {
+      std::vector<double> sg((size_t)r, 1.0);
+      for (int64_t c = 0; c < r; ++c) {
+        int mx = 0;
+        for (int64_t k = 0; k < K; ++k) mx = std::max(mx, std::abs((int)qu[k * r + c]));
+        const double bound = 2.0 * su[c] * (double)K * (double)(a.qmax - a.qmin) * (double)mx;
+        sg[c] = bound > 0 ? pow2_ceil(bound / 32768.0) : 1.0;
+      }
+      return sg;
+    };
+    std::vector<double> sig_s, sig_c;
+    if (L->r_s) {
+      if ((rc = check_codes(d->q_us, K * L->r_s, waux, "q_us")) ||
+          (rc = check_codes(d->q_vs, L->r_s * N, waux, "q_vs")))
+        return cleanup(rc);
+      sig_s = sigmas(d->q_us, d->s_us, L->r_s, act);
+      if ((rc = pack_weight(L, d->q_us, d->s_us, K, L->r_s, L->ld_main, &L->b_us, &L->s_us,
+                            &L->cs_us, 1.0, &sig_s)))
+        return cleanup(rc);
+    }
+    if (L->r_c) {
+      if ((rc = check_codes(d->q_uc, K * L->r_c, waux, "q_uc")) ||
+          (rc = check_codes(d->q_vc, L->r_c * N, waux, "q_vc")))
+        return cleanup(rc);
+      sig_c = sigmas(d->q_uc, d->s_uc, L->r_c, aux);
+      if ((rc = pack_weight(L, d->q_uc, d->s_uc, K, L->r_c, L->ld_main, &L->b_uc, &L->s_uc,
+                            &L->cs_uc, 1.0, &sig_c)))
+        return cleanup(rc);
+    }
+    std::vector<__half> blr((size_t)N * L->k_lr, __float2half(0.f));
+    std::vector<float> kap((size_t)N);
+    std::vector<double> row((size_t)L->k_lr);
+    for (int64_t j = 0; j < N; ++j) {
+      const double colf = L->r_s ? d->s_vs[j] : d->s_vc[j];
+      std::fill(row.begin(), row.end(), 0.0);
+      double mx = 0.0;
+      for (int64_t c = 0; c < L->r_s; ++c) {
+        row[c] = (double)d->q_vs[c * N + j] * sig_s[c];
+        mx = std::max(mx, std::fabs(row[c]));
+      }
+      for (int64_t c = 0; c < L->r_c; ++c) {
+        row[L->r_s16 + c] = (double)d->q_vc[c * N + j] * (d->s_vc[j] / colf) * sig_c[c];
+        mx = std::max(mx, std::fabs(row[L->r_s16 + c]));
+      }
+      const double kappa = mx > 0 ? pow2_ceil(mx) : 1.0;
+      for (int64_t c = 0; c < L->k_lr; ++c)
+        blr[(size_t)j * L->k_lr + c] = __double2half(row[c] / kappa);
+      kap[j] = (float)(kappa * colf);
+    }
+    if ((rc = L->mem.upload(&L->b_lr, blr.data(), blr.size()))) return cleanup(rc);
+    if ((rc = L->mem.upload(&L->kappa, kap.data(), kap.size()))) return cleanup(rc);
+  }
+  *out = L;
+  return SPLITQ_OK;
+}
+
+int splitq_layer_destroy(splitq_layer_t L) {
+  if (!L) return SPLITQ_OK;
+  cudaSetDevice(L->device);
+  L->mem.release();
+  delete L;
+  return SPLITQ_OK;
+}
+
+int splitq_workspace_layout(splitq_layer_t L, int64_t T, splitq_ws_layout_t* o) {
+  if (!L || !o) return fail(SPLITQ_ERR_INVALID, "null argument");
+  if (T <= 0) return fail(SPLITQ_ERR_INVALID, "batch must contain at least one token");
+  std::memset(o, 0xff, sizeof(*o));  // -1 everywhere
+  int64_t off = 0;
+  auto take = [&](int64_t bytes) {
+    const int64_t at = off;
+    off = round_up(off + bytes, 256);
+    return at;
+  };
+  o->status = take(16);
+  o->n_text = take(16);
+  o->text_idx = take(4 * T);
+  o->text_rows = take(4 * T);
+  o->ld_main = L->ld_main;
+  o->a_main = take(T * L->ld_main);
+  o->s_main = take(8 * T);
+  o->sf_main = take(4 * T);
+  o->zp_main = take(4 * T);
+  o->lrs_main = take(4 * T);
+  o->rho = take(4 * T);
+  o->ld_text = L->ld_text;
+  o->ld_vision = L->ld_vis;
+  if (L->n_text) {
+    o->a_text = take(T * L->ld_text);
+    o->s_text = take(8 * T);
+    o->sf_text = take(4 * T);
+    o->zp_text = take(4 * T);
+  }
+  if (L->n_vis) {
+    o->a_vision = take(T * L->ld_vis);
+    o->s_vision = take(8 * T);
+    o->sf_vision = take(4 * T);
+    o->zp_vision = take(4 * T);
+  }
+  if (L->use_mac) {
+    o->a_mac = take(T * L->ld_main);
+    o->s_mac = take(8 * T);
+    o->zp_mac = take(4 * T);
+    o->lrs_mac = take(4 * T);
+  }
+  o->k_lr = L->k_lr;
+  if (L->k_lr) o->lr_a = take(2 * T * L->k_lr);
+  o->total_bytes = off;
+  o->code_centered_main = L->act.centered;
+  o->code_centered_aux = L->aux.centered;
+  return SPLITQ_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+bool g_gemm_attr_set[64] = {false};
+
+struct GemmLaunch {
+  GemmMaps maps;
+  GemmParams p;
+};
+
+int launch_gemm(GemmLaunch& g, int device, int64_t max_rows, cudaStream_t stream) {
+  if (device >= 0 && device < 64 && !g_gemm_attr_set[device]) {
+    CUDA_TRY(cudaFuncSetAttribute(splitq_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  GEMM_SMEM_BYTES));
+    g_gemm_attr_set[device] = true;
+  }
+  const int64_t m_tiles = (max_rows + GEMM_BM - 1) / GEMM_BM;
+  const int64_t n_tiles = (g.p.N + g.p.bn - 1) / g.p.bn;
+  const int64_t tiles = m_tiles * n_tiles;
+  if (tiles == 0) return SPLITQ_OK;
+  const int grid = (int)std::min<int64_t>(tiles, sm_count(device));
+  splitq_gemm_kernel<<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, stream>>>(g.maps, g.p);
+  CUDA_TRY(cudaGetLastError());
+  return SPLITQ_OK;
+}
+
+bool map_i8(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld,
+            uint32_t box_rows) {
+  return make_map_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, rows, cols, ld, box_rows, 128);
+}
+bool map_f16(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld_elems,
+             uint32_t box_rows) {
+  return make_map_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, rows, cols, ld_elems * 2, box_rows,
+                     64);
+}
+
+int tile_n(int64_t n) { return (int)std::min<int64_t>(GEMM_MAX_BN, round_up(n, 16)); }
+
+}  // namespace
+
+extern "C" {
+
+int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, const uint8_t* tags,
+                   int64_t T, void* y, int y_dtype, int64_t y_ld, void* ws, size_t ws_bytes,
+                   void* stream_, int flags) {
+  if (!L || !x || !tags || !y || !ws) return fail(SPLITQ_ERR_INVALID, "null argument");
+  if (T <= 0) return fail(SPLITQ_ERR_INVALID, "batch must contain at least one token");
+  if (T > (int64_t)1 << 30) return fail(SPLITQ_ERR_INVALID, "too many tokens");
+  if (x_dtype < 0 || x_dtype > 3) return fail(SPLITQ_ERR_INVALID, "bad x dtype");
+  if (x_ld < L->d_in) return fail(SPLITQ_ERR_INVALID, "batch width does not match partition dim");
+  const bool raw = (flags & SPLITQ_FWD_RAW) != 0;
+  if (!raw && (y_dtype != SPLITQ_F32 && y_dtype != SPLITQ_F16 && y_dtype != SPLITQ_BF16))
+    return fail(SPLITQ_ERR_INVALID, "bad y dtype");
+  if (y_ld < L->d_out) return fail(SPLITQ_ERR_INVALID, "y leading dimension too small");
+  splitq_ws_layout_t W;
+  int rc = splitq_workspace_layout(L, T, &W);
+  if (rc) return rc;
+  if ((int64_t)ws_bytes < W.total_bytes)
+    return fail(SPLITQ_ERR_INVALID, "workspace too small (%zu < %lld)", ws_bytes,
+                (long long)W.total_bytes);
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0)
+    return fail(SPLITQ_ERR_INVALID, "workspace must be 256-byte aligned");
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  uint8_t* base = reinterpret_cast<uint8_t*>(ws);
+  auto at = [&](int64_t off) -> void* { return off < 0 ? nullptr : base + off; };
+  int* err = (int*)at(W.status);
+  int* n_text = (int*)at(W.n_text);
+  int* text_idx = (int*)at(W.text_idx);
+  int* text_rows = (int*)at(W.text_rows);
+
+  CUDA_TRY(cudaMemsetAsync(err, 0, 16, stream));
+  compact_text_rows_kernel<<<1, 1024, 0, stream>>>(tags, (int)T, text_idx, text_rows, n_text, err);
+  CUDA_TRY(cudaGetLastError());
+
+  K1Params k{};
+  k.x = x;
+  k.x_dtype = x_dtype;
+  k.ldx = x_ld;
+  k.T = (int)T;
+  k.c_main = L->c_main;
+  k.d_main = L->d_main;
+  k.n_main = (int)L->n_main;
+  k.ld_main = (int)L->ld_main;
+  k.act = L->act;
+  k.aux = L->aux;
+  k.a_main = (int8_t*)at(W.a_main);
+  k.s_main = (double*)at(W.s_main);
+  k.sf_main = (float*)at(W.sf_main);
+  k.zp_main = (int*)at(W.zp_main);
+  k.lrs_main = (float*)at(W.lrs_main);
+  k.rho = (float*)at(W.rho);
+  k.c_text = L->c_text;
+  k.d_text = L->d_text;
+  k.n_text = (int)L->n_text;
+  k.ld_text = (int)L->ld_text;
+  k.a_text = (int8_t*)at(W.a_text);
+  k.s_text = (double*)at(W.s_text);
+  k.sf_text = (float*)at(W.sf_text);
+  k.zp_text = (int*)at(W.zp_text);
+  k.c_vis = L->c_vis;
+  k.d_vis = L->d_vis;
+  k.n_vis = (int)L->n_vis;
+  k.ld_vis = (int)L->ld_vis;
+  k.a_vis = (int8_t*)at(W.a_vision);
+  k.s_vis = (double*)at(W.s_vision);
+  k.sf_vis = (float*)at(W.sf_vision);
+  k.zp_vis = (int*)at(W.zp_vision);
+  k.use_mac = L->use_mac;
+  k.text_idx = text_idx;
+  k.a_mac = (int8_t*)at(W.a_mac);
+  k.s_mac = (double*)at(W.s_mac);
+  k.zp_mac = (int*)at(W.zp_mac);
+  k.lrs_mac = (float*)at(W.lrs_mac);
+  k.lr_a = (__half*)at(W.lr_a);
+  k.k_lr = (int)L->k_lr;
+  k.err = err;
+  k1_quantize_kernel<<<(unsigned)T, K1_THREADS, 0, stream>>>(k);
+  CUDA_TRY(cudaGetLastError());
+
+  const uint32_t a_fmt_main = L->act.centered ? 1u : 0u;  // s8 : u8
+  const uint32_t a_fmt_aux = L->aux.centered ? 1u : 0u;
+  __half* lr_a = (__half*)at(W.lr_a);
+
+  // ---- low-rank first stages (write the fp16 second-stage operand)
+  if (L->r_s) {
+    GemmLaunch g{};
+    g.p.M = (int)T;
+    g.p.N = (int)L->r_s;
+    g.p.bn = tile_n(L->r_s);
+    g.p.k_main = (int)L->n_main;
+    g.p.idesc_main = make_idesc(2, a_fmt_main, 1, GEMM_BM, g.p.bn);
+    g.p.mode = EPI_LR1;
+    g.p.row_s = (const float*)at(W.lrs_main);
+    g.p.row_zp = L->act.centered ? nullptr : (const int*)at(W.zp_main);
+    g.p.col_s = L->s_us;
+    g.p.col_cs = L->cs_us;
+    g.p.out = lr_a;
+    g.p.ldo = L->k_lr;
+    g.p.col_off = 0;
+    g.p.err = err;
+    bool ok = map_i8(&g.maps.a, at(W.a_main), T, L->n_main, L->ld_main, GEMM_BM) &&
+              map_i8(&g.maps.b, L->b_us, L->r_s, L->n_main, L->ld_main, g.p.bn);
+    g.maps.at = g.maps.bt = g.maps.av = g.maps.bv = g.maps.la = g.maps.lb = g.maps.a;
+    if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (LR1 cws)");
+    if ((rc = launch_gemm(g, L->device, T, stream))) return rc;
+  }
+  if (L->r_c) {
+    GemmLaunch g{};
+    g.p.M = (int)T;
+    g.p.m_count = n_text;
+    g.p.N = (int)L->r_c;
+    g.p.bn = tile_n(L->r_c);
+    g.p.k_main = (int)L->n_main;
+    g.p.idesc_main = make_idesc(2, a_fmt_aux, 1, GEMM_BM, g.p.bn);
+    g.p.mode = EPI_LR1;
+    g.p.row_s = (const float*)at(W.lrs_mac);
+    g.p.row_zp = L->aux.centered ? nullptr : (const int*)at(W.zp_mac);
+    g.p.col_s = L->s_uc;
+    g.p.col_cs = L->cs_uc;
+    g.p.out = lr_a;
+    g.p.ldo = L->k_lr;
+    g.p.col_off = (int)L->r_s16;
+    g.p.row_map = text_rows;
+    g.p.err = err;
+    bool ok = map_i8(&g.maps.a, at(W.a_mac), T, L->n_main, L->ld_main, GEMM_BM) &&
+              map_i8(&g.maps.b, L->b_uc, L->r_c, L->n_main, L->ld_main, g.p.bn);
+    g.maps.at = g.maps.bt = g.maps.av = g.maps.bv = g.maps.la = g.maps.lb = g.maps.a;
+    if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (LR1 mac)");
+    if ((rc = launch_gemm(g, L->device, T, stream))) return rc;
+  }
+
+  // ---- split GEMM: main + outliers + low-rank second stage + merge
+  GemmLaunch g{};
+  g.p.M = (int)T;
+  g.p.N = (int)L->d_out;
+  g.p.bn = tile_n(L->d_out);
+  g.p.k_main = (int)L->n_main;
+  g.p.k_text = (int)L->n_text;
+  g.p.k_vis = (int)L->n_vis;
+  g.p.k_lr = (int)L->k_lr;
+  g.p.idesc_main = make_idesc(2, a_fmt_main, 1, GEMM_BM, g.p.bn);
+  g.p.idesc_text = make_idesc(2, a_fmt_aux, 1, GEMM_BM, g.p.bn);
+  g.p.idesc_vis = g.p.idesc_text;
+  g.p.idesc_lr = make_idesc(1, 0, 0, GEMM_BM, g.p.bn);
+  g.p.mode = raw ? EPI_RAW : EPI_SPLIT;
+  g.p.out_dtype = y_dtype == SPLITQ_F32 ? OUT_F32 : y_dtype == SPLITQ_F16 ? OUT_F16 : OUT_BF16;
+  g.p.row_s = (const float*)at(W.sf_main);
+  g.p.row_zp = L->act.centered ? nullptr : (const int*)at(W.zp_main);
+  g.p.row_st = (const float*)at(W.sf_text);
+  g.p.row_zpt = L->aux.centered ? nullptr : (const int*)at(W.zp_text);
+  g.p.row_sv = (const float*)at(W.sf_vision);
+  g.p.row_zpv = L->aux.centered ? nullptr : (const int*)at(W.zp_vision);
+  g.p.row_rho = (const float*)at(W.rho);
+  g.p.col_s = L->s_main;
+  g.p.col_cs = L->cs_main;
+  g.p.col_st = L->s_text;
+  g.p.col_cst = L->cs_text;
+  g.p.col_sv = L->s_vis;
+  g.p.col_csv = L->cs_vis;
+  g.p.col_kappa = L->kappa;
+  g.p.out = y;
+  g.p.ldo = y_ld;
+  if (raw) {
+    int* planes = reinterpret_cast<int*>(y);
+    const int64_t plane = T * y_ld;
+    g.p.raw_t = planes + plane;
+    g.p.raw_v = planes + 2 * plane;
+    g.p.raw_f = reinterpret_cast<float*>(planes + 3 * plane);
+  }
+  bool ok = map_i8(&g.maps.a, at(W.a_main), T, L->n_main, L->ld_main, GEMM_BM) &&
+            map_i8(&g.maps.b, L->b_main, L->d_out, L->n_main, L->ld_main, g.p.bn);
+  g.maps.at = g.maps.bt = g.maps.av = g.maps.bv = g.maps.la = g.maps.lb = g.maps.a;
+  if (ok && L->n_text)
+    ok = map_i8(&g.maps.at, at(W.a_text), T, L->n_text, L->ld_text, GEMM_BM) &&
+         map_i8(&g.maps.bt, L->b_text, L->d_out, L->n_text, L->ld_text, g.p.bn);
+  if (ok && L->n_vis)
+    ok = map_i8(&g.maps.av, at(W.a_vision), T, L->n_vis, L->ld_vis, GEMM_BM) &&
+         map_i8(&g.maps.bv, L->b_vis, L->d_out, L->n_vis, L->ld_vis, g.p.bn);
+  if (ok && L->k_lr)
+    ok = map_f16(&g.maps.la, lr_a, T, L->k_lr, L->k_lr, GEMM_BM) &&
+         map_f16(&g.maps.lb, L->b_lr, L->d_out, L->k_lr, L->k_lr, g.p.bn);
+  if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (split GEMM)");
+  return launch_gemm(g, L->device, T, stream);
+}
+
+int splitq_read_status(void* ws, void* stream_, int32_t* status_out) {
+  if (!ws) return fail(SPLITQ_ERR_INVALID, "null workspace");
+  int32_t st = 0;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  CUDA_TRY(cudaMemcpyAsync(&st, ws, sizeof(st), cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  if (status_out) *status_out = st;
+  if (st & SPLITQ_STATUS_NONFINITE) return fail(SPLITQ_ERR_DATA, "non-finite value in matrix");
+  if (st & SPLITQ_STATUS_SCALE) return fail(SPLITQ_ERR_DATA, "scales must be positive");
+  if (st & SPLITQ_STATUS_TAG) return fail(SPLITQ_ERR_DATA, "tags must be 0 (text) or 1 (vision)");
+  if (st & SPLITQ_STATUS_LR_RANGE)
+    return fail(SPLITQ_ERR_DATA, "low-rank operand exceeded the fp16 range");
+  return SPLITQ_OK;
+}
+
+int splitq_quantize_rows(const void* x, int x_dtype, int64_t x_ld, int64_t rows, int64_t cols,
+                         splitq_qspec_t spec, int8_t* codes, int64_t codes_ld, double* scales,
+                         int32_t* zero_points, int32_t* status, int32_t* centered_out,
+                         void* stream_) {
+  if (!x || !codes || !scales || !zero_points || !status)
+    return fail(SPLITQ_ERR_INVALID, "null argument");
+  if (rows <= 0 || cols <= 0) return fail(SPLITQ_ERR_INVALID, "empty matrix");
+  if (codes_ld < cols || (codes_ld & 3)) return fail(SPLITQ_ERR_INVALID, "codes_ld must be >= cols and a multiple of 4");
+  QSpecDev s;
+  int rc = make_spec(spec, &s, "spec");
+  if (rc) return rc;
+  if (centered_out) *centered_out = s.centered;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), stream));
+  K1Params k{};
+  k.x = x;
+  k.x_dtype = x_dtype;
+  k.ldx = x_ld;
+  k.T = (int)rows;
+  k.n_main = (int)cols;
+  k.ld_main = (int)codes_ld;
+  k.act = s;
+  k.aux = s;
+  k.a_main = codes;
+  k.s_main = scales;
+  k.zp_main = zero_points;
+  k.err = status;
+  k1_quantize_kernel<<<(unsigned)rows, K1_THREADS, 0, stream>>>(k);
+  CUDA_TRY(cudaGetLastError());
+  return SPLITQ_OK;
+}
+
+int splitq_gemm_i8(const int8_t* a, int64_t lda, int a_signed, const int8_t* b, int64_t ldb,
+                   int32_t* c, int64_t ldc, int64_t m, int64_t n, int64_t k, void* stream_) {
+  if (!a || !b || !c) return fail(SPLITQ_ERR_INVALID, "null argument");
+  if (m <= 0 || n <= 0 || k <= 0) return fail(SPLITQ_ERR_INVALID, "empty GEMM");
+  if ((lda & 15) || (ldb & 15) || lda < k || ldb < k)
+    return fail(SPLITQ_ERR_INVALID, "lda/ldb must be >= k and multiples of 16");
+  int device = 0;
+  CUDA_TRY(cudaGetDevice(&device));
+  GemmLaunch g{};
+  g.p.M = (int)m;
+  g.p.N = (int)n;
+  g.p.bn = tile_n(n);
+  g.p.k_main = (int)k;
+  g.p.idesc_main = make_idesc(2, a_signed ? 1u : 0u, 1, GEMM_BM, g.p.bn);
+  g.p.mode = EPI_RAW;
+  g.p.out = c;
+  g.p.ldo = ldc;
+  bool ok = map_i8(&g.maps.a, a, m, k, lda, GEMM_BM) && map_i8(&g.maps.b, b, n, k, ldb, g.p.bn);
+  g.maps.at = g.maps.bt = g.maps.av = g.maps.bv = g.maps.la = g.maps.lb = g.maps.a;
+  if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  return launch_gemm(g, device, m, reinterpret_cast<cudaStream_t>(stream_));
+}
+
+}  // extern "C"
