@@ -1,1 +1,39 @@
-"""B200-native SplitQ split-linear hot path (package stub, API lands next)."""
+"""B200-native (sm_100a) SplitQ split-linear hot path.
+
+Drop-in for the hot-path subset of the reference package ``modquant``
+(pkg/src/modquant/__init__.py): same names and semantics, with the forward,
+the per-token activation quantizer and the MOCD calibration statistics
+running as hand-written CUDA kernels behind the C-ABI in include/splitq.h.
+"""
+
+from .layer import (
+    AUX_BITS_FLOOR,
+    DEFAULT_ACT_SPEC,
+    DEFAULT_WEIGHT_SPEC,
+    SplitLayer,
+    build_layer,
+    forward,
+    forward_reference,
+)
+from .lowrank import LowRankBranch, SvdFactors, build_branch, default_rank, truncated_svd
+from .mocd import ChannelPartition, MocdConfig, select_topk, trivial_partition
+from .quantizer import (
+    Granularity,
+    QuantParams,
+    QuantSpec,
+    compute_params,
+    fake_quantize,
+    quantize,
+    quantize_per_token,
+)
+from .tensor import ActivationBatch, ModalityTag
+from .transform import Transform, diagonal_transform, identity_transform, init_transform
+
+__all__ = [
+    "AUX_BITS_FLOOR", "DEFAULT_ACT_SPEC", "DEFAULT_WEIGHT_SPEC", "SplitLayer", "build_layer",
+    "forward", "forward_reference", "LowRankBranch", "SvdFactors", "build_branch",
+    "default_rank", "truncated_svd", "ChannelPartition", "MocdConfig", "select_topk",
+    "trivial_partition", "Granularity", "QuantParams", "QuantSpec", "compute_params",
+    "fake_quantize", "quantize", "quantize_per_token", "ActivationBatch", "ModalityTag",
+    "Transform", "diagonal_transform", "identity_transform", "init_transform",
+]

@@ -1,0 +1,253 @@
+"""Device runtime: layer packing, workspace management and the launches.
+
+torch is used only as plumbing (device memory, the current CUDA stream);
+every computation on the path runs in libsplitq_b200.so. There is no CPU
+fallback: without a CUDA device or the native library these functions
+raise.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+
+import numpy as np
+
+from . import _lib
+from .quantizer import QuantParams, weight_codes
+from .tensor import _is_torch
+
+_DTYPES = None
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def device():
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2605_19929_b200 needs a CUDA device (sm_100a); no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _dtype_code(t):
+    torch = _torch()
+    return {torch.float16: _lib.F16, torch.float32: _lib.F32, torch.float64: _lib.F64,
+            torch.bfloat16: _lib.BF16}[t]
+
+
+def _stream():
+    return C.c_void_p(_torch().cuda.current_stream().cuda_stream)
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(C.c_void_p)
+    return C.c_void_p(a.data_ptr())
+
+
+def _spec_struct(spec):
+    if spec.bits is None or not 2 <= spec.bits <= 8:
+        raise ValueError(
+            f"the GPU split-linear path supports 2..8-bit integer specs (got bits={spec.bits}); "
+            "identity / wide specs stay on the CPU reference")
+    return _lib.QSpec(int(spec.bits), int(bool(spec.symmetric)))
+
+
+def _gran(spec):
+    g = spec.granularity
+    return getattr(g, "value", g)
+
+
+class GpuLayer:
+    """A SplitLayer packed on one device: the C handle plus its geometry."""
+
+    def __init__(self, layer, dev=None):
+        lib = _lib.load()
+        dev = dev or device()
+        if _gran(layer.act_spec) != "per_token":
+            raise ValueError("activation spec must be PER_TOKEN on the GPU path")
+        if _gran(layer.weight_spec) == "per_token":
+            raise ValueError("weight spec must be PER_CHANNEL or PER_TENSOR on the GPU path")
+        p = layer.partition
+        d_out = int(np.asarray(layer.w_main).shape[1])
+        act, wsp = _spec_struct(layer.act_spec), _spec_struct(layer.weight_spec)
+        floor = int(layer.aux_bits_floor)
+        w_aux = layer.weight_spec.with_floor(floor)
+        _spec_struct(w_aux)
+        keep = []
+
+        def arr(a, dt):
+            a = np.ascontiguousarray(np.asarray(a), dtype=dt)
+            keep.append(a)
+            return a
+
+        d_main = arr(layer.p_main.scale, np.float64)
+        d_text = arr(layer.p_text.scale, np.float64) if len(p.c_text) else arr(np.zeros(0), np.float64)
+        d_vis = arr(layer.p_vision.scale, np.float64) if len(p.c_vision) else arr(np.zeros(0), np.float64)
+        # weight side of forward_with_cache (layer.py:137-163), once
+        w_main = np.asarray(layer.w_main, np.float64)
+        w_prime = w_main / d_main[:, np.newaxis]  # apply_inv_left (transform.py:106-115)
+        desc = _lib.LayerDesc()
+        desc.d_in, desc.d_out = int(p.dim), d_out
+        desc.n_main, desc.n_text, desc.n_vision = len(p.c_main), len(p.c_text), len(p.c_vision)
+        desc.c_main = _ptr(arr(p.c_main, np.int64))
+        desc.c_text = _ptr(arr(p.c_text, np.int64))
+        desc.c_vision = _ptr(arr(p.c_vision, np.int64))
+        desc.scale_main, desc.scale_text, desc.scale_vision = _ptr(d_main), _ptr(d_text), _ptr(d_vis)
+        desc.act, desc.weight, desc.aux_bits_floor = act, wsp, floor
+        desc.use_cws, desc.use_mac = int(bool(layer.use_cws)), int(bool(layer.use_mac))
+
+        def put(name, m, spec):
+            q, s = weight_codes(m, spec)
+            setattr(desc, "q_" + name, _ptr(arr(q, np.int8)))
+            setattr(desc, "s_" + name, _ptr(arr(s, np.float64)))
+
+        if layer.use_cws:
+            br = layer.branch_smooth
+            v_eff = br.effective_v()
+            r_pre = w_prime - br.u_star @ v_eff  # layer.py:144 (same numpy/BLAS call)
+            put("main", r_pre, layer.weight_spec)
+            put("us", br.u_star, w_aux)
+            put("vs", v_eff, w_aux)
+            desc.r_cws = int(br.rank)
+        else:
+            put("main", w_prime, layer.weight_spec)
+        if layer.use_mac:
+            br = layer.branch_comp
+            put("uc", br.u_star, w_aux)
+            put("vc", br.effective_v(), w_aux)
+            desc.r_mac = int(br.rank)
+        if len(p.c_text):
+            put("text", np.asarray(layer.w_text, np.float64) / d_text[:, np.newaxis], w_aux)
+        if len(p.c_vision):
+            put("vision", np.asarray(layer.w_vision, np.float64) / d_vis[:, np.newaxis], w_aux)
+        handle = C.c_void_p()
+        _lib.check(lib.splitq_layer_create(C.byref(desc), int(dev.index or 0), C.byref(handle)))
+        self.handle = handle
+        self.device = dev
+        self.d_in, self.d_out = int(p.dim), d_out
+        self._ws = {}
+        self._finalizer = weakref.finalize(self, lib.splitq_layer_destroy, handle)
+
+    def layout(self, tokens: int) -> _lib.WsLayout:
+        lay = _lib.WsLayout()
+        _lib.check(_lib.load().splitq_workspace_layout(self.handle, int(tokens), C.byref(lay)))
+        return lay
+
+    def workspace(self, tokens: int):
+        torch = _torch()
+        ws = self._ws.get(tokens)
+        if ws is None:
+            lay = self.layout(tokens)
+            ws = torch.empty(int(lay.total_bytes), dtype=torch.uint8, device=self.device)
+            self._ws = {tokens: ws}  # keep the latest size only
+        return ws
+
+    def run(self, x, tags, y=None, out_dtype=None, raw=False, check=True, ws=None):
+        """Launch the forward on the current stream. x: CUDA [T x >=d_in]
+        (f16/bf16/f32/f64, unit column stride), tags: CUDA uint8 [T]."""
+        torch = _torch()
+        lib = _lib.load()
+        T = int(x.shape[0])
+        if x.shape[1] != self.d_in:
+            raise ValueError("batch width does not match partition dim")
+        if x.stride(1) != 1:
+            x = x.contiguous()
+        tags = tags.to(torch.uint8)
+        if ws is None:
+            ws = self.workspace(T)
+        if raw:
+            y = torch.empty((4, T, self.d_out), dtype=torch.int32, device=self.device)
+            ydt = _lib.F32
+        else:
+            out_dtype = out_dtype or torch.float32
+            if y is None:
+                y = torch.empty((T, self.d_out), dtype=out_dtype, device=self.device)
+            ydt = _dtype_code(y.dtype)
+        y_ld = y.stride(-2)
+        _lib.check(lib.splitq_forward(self.handle, _ptr(x), _dtype_code(x.dtype), x.stride(0),
+                                      _ptr(tags), T, _ptr(y), ydt, y_ld, _ptr(ws),
+                                      ws.numel(), _stream(), _lib.FWD_RAW if raw else 0))
+        if check:
+            st = C.c_int32()
+            _lib.check(lib.splitq_read_status(_ptr(ws), _stream(), C.byref(st)))
+        return y
+
+
+_PACKED: dict = {}
+
+
+def packed(layer) -> GpuLayer:
+    """Pack a layer once per (object, device); the cache entry dies with it."""
+    if isinstance(layer, GpuLayer):
+        return layer
+    dev = device()
+    key = (id(layer), dev.index)
+    g = _PACKED.get(key)
+    if g is None:
+        g = GpuLayer(layer, dev)
+        _PACKED[key] = g
+        try:
+            weakref.finalize(layer, _PACKED.pop, key, None)
+        except TypeError:  # object without weakref support: keep it
+            pass
+    return g
+
+
+def forward(layer, batch, out_dtype=None):
+    torch = _torch()
+    g = packed(layer)
+    dev = g.device
+    data, tags = batch.data, batch.tags
+    if _is_torch(data):
+        x = data.to(dev)
+        t = tags.to(dev) if _is_torch(tags) else torch.as_tensor(np.asarray(tags, np.uint8), device=dev)
+        return g.run(x, t, out_dtype=out_dtype)
+    x = torch.from_numpy(np.ascontiguousarray(data, dtype=np.float64)).to(dev)
+    t = torch.from_numpy(np.ascontiguousarray(tags, dtype=np.uint8)).to(dev)
+    y = g.run(x, t, out_dtype=torch.float32)
+    return y.cpu().numpy().astype(np.float64)
+
+
+def quantize_rows(x, spec):
+    """PER_TOKEN quantization on the GPU -> (codes q int64 ndarray, QuantParams)."""
+    torch = _torch()
+    lib = _lib.load()
+    dev = device()
+    host = not _is_torch(x)
+    if host:
+        xa = np.asarray(x, dtype=np.float64)
+        if xa.ndim != 2:
+            raise ValueError(f"matrix must be 2-D, got ndim={xa.ndim}")
+        xt = torch.from_numpy(np.ascontiguousarray(xa)).to(dev)
+    else:
+        xt = x.to(dev)
+        if xt.ndim != 2:
+            raise ValueError(f"matrix must be 2-D, got ndim={xt.ndim}")
+        if xt.stride(1) != 1:
+            xt = xt.contiguous()
+    rows, cols = int(xt.shape[0]), int(xt.shape[1])
+    if rows == 0 or cols == 0:
+        return np.zeros((rows, cols), np.int64), QuantParams(np.ones(rows), np.zeros(rows, np.int64))
+    ld = (cols + 15) // 16 * 16
+    codes = torch.empty((rows, ld), dtype=torch.int8, device=dev)
+    scales = torch.empty(rows, dtype=torch.float64, device=dev)
+    zps = torch.empty(rows, dtype=torch.int32, device=dev)
+    status = torch.zeros(4, dtype=torch.int32, device=dev)
+    centered = C.c_int32()
+    _lib.check(lib.splitq_quantize_rows(_ptr(xt), _dtype_code(xt.dtype), xt.stride(0), rows, cols,
+                                        _spec_struct(spec), _ptr(codes), ld, _ptr(scales),
+                                        _ptr(zps), _ptr(status), C.byref(centered), _stream()))
+    st = C.c_int32()
+    _lib.check(lib.splitq_read_status(_ptr(status), _stream(), C.byref(st)))
+    s = scales.cpu().numpy()
+    z = zps.cpu().numpy().astype(np.int64)
+    c = codes[:, :cols].cpu().numpy().astype(np.int64)
+    q = c + z[:, None] if centered.value else (c & 0xFF)
+    return q, QuantParams(s, z)

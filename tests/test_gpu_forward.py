@@ -1,0 +1,268 @@
+"""GPU parity of the split-linear forward against the CPU oracle.
+
+Bars (BASELINE.json north star):
+  * activation codes, scales and zero points: bit-exact (scales as fp64);
+  * int32 main / text / vision accumulators: bit-exact;
+  * fp32 output: max |y_gpu - y_ref| <= 1e-3 * rms(y_ref).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import workloads as wl
+from oracle import splitq_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3  # of the output RMS (north star)
+
+
+def _pkg():
+    import paper_2605_19929_b200 as pkg
+    return pkg
+
+
+def _case(seed, T, d_in, d_out, k_t, k_v, r_s, r_c, abits=4, wbits=4, a_sym=False,
+          n_vision=None, x_dtype=np.float32, scale=(30.0, 100.0)):
+    pkg = _pkg()
+    rng = np.random.default_rng(seed)
+    if n_vision is None:
+        n_vision = T // 4
+    tags = wl.tags_with_spans(rng, T, n_vision)
+    c_t, c_v = wl.outlier_sets(rng, d_in, max(k_t, k_v))
+    c_t, c_v = c_t[:k_t], c_v[:k_v]
+    x = wl.make_activations(rng, T, d_in, tags, c_t, c_v, *scale, dtype=x_dtype)
+    col_max = np.max(np.abs(x.astype(np.float64)), axis=0)
+    spec = wl.LayerSpec("t", d_in, d_out, k_t, k_v, r_s, r_c, abits, wbits, a_sym)
+    layer = wl.build_split_layer(pkg, rng, spec, col_max, c_t, c_v)
+    return layer, x, tags
+
+
+def _ws_view(ws, off, dtype, count):
+    nbytes = np.dtype(dtype).itemsize * count
+    return ws[off: off + nbytes].cpu().numpy().view(dtype)
+
+
+def _run_gpu(layer, x, tags, raw=False):
+    from paper_2605_19929_b200 import runtime
+    g = runtime.packed(layer)
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    td = torch.from_numpy(tags).cuda()
+    ws = g.workspace(x.shape[0])
+    y = g.run(xd, td, raw=raw, ws=ws)
+    torch.cuda.synchronize()
+    return g, ws, y
+
+
+def _check_codes(layer, x, tags):
+    L = orc.from_reference_layer(layer)
+    act = orc.activation_codes(L, x.astype(np.float64), tags)
+    g, ws, _ = _run_gpu(layer, x, tags)
+    lay = g.layout(x.shape[0])
+    T = x.shape[0]
+    cen_m, cen_a = lay.code_centered_main, lay.code_centered_aux
+
+    def codes_of(off, ld, rows, cols, centered, zp):
+        c = _ws_view(ws, off, np.int8, rows * ld).reshape(rows, ld)[:, :cols].astype(np.int64)
+        return c + zp[:, None] if centered else (c & 0xFF)
+
+    q, s, z = act["main"]
+    zp = _ws_view(ws, lay.zp_main, np.int32, T).astype(np.int64)
+    np.testing.assert_array_equal(zp, z)
+    np.testing.assert_array_equal(_ws_view(ws, lay.s_main, np.float64, T), s)
+    np.testing.assert_array_equal(codes_of(lay.a_main, lay.ld_main, T, q.shape[1], cen_m, zp), q)
+    for name, off_a, off_s, off_z, ld in (("text", lay.a_text, lay.s_text, lay.zp_text, lay.ld_text),
+                                          ("vision", lay.a_vision, lay.s_vision, lay.zp_vision,
+                                           lay.ld_vision)):
+        if name not in act:
+            continue
+        q, s, z = act[name]
+        zp = _ws_view(ws, off_z, np.int32, T).astype(np.int64)
+        np.testing.assert_array_equal(zp, z)
+        np.testing.assert_array_equal(_ws_view(ws, off_s, np.float64, T), s)
+        np.testing.assert_array_equal(codes_of(off_a, ld, T, q.shape[1], cen_a, zp), q)
+    if "mac" in act:
+        q, s, z = act["mac"]
+        n = q.shape[0]
+        assert int(_ws_view(ws, lay.n_text, np.int32, 1)[0]) == n
+        np.testing.assert_array_equal(_ws_view(ws, lay.text_rows, np.int32, n), act["text_rows"])
+        zp = _ws_view(ws, lay.zp_mac, np.int32, n).astype(np.int64)
+        np.testing.assert_array_equal(zp, z)
+        np.testing.assert_array_equal(_ws_view(ws, lay.s_mac, np.float64, n), s)
+        np.testing.assert_array_equal(codes_of(lay.a_mac, lay.ld_main, n, q.shape[1], cen_a, zp), q)
+
+
+def _check_acc(layer, x, tags):
+    L = orc.from_reference_layer(layer)
+    acc = orc.accumulators(L, x.astype(np.float64), tags)
+    act = orc.activation_codes(L, x.astype(np.float64), tags)
+    w = orc.weight_codes(L)
+    g, _, y = _run_gpu(layer, x, tags, raw=True)
+    lay = g.layout(x.shape[0])
+    planes = y.cpu().numpy().astype(np.int64)
+    T = x.shape[0]
+
+    def expect(name, centered):
+        # u8 (non-centred) codes: the tensor core accumulates q * w; the zero
+        # point term zp * colsum(w) is removed in the epilogue
+        if centered:
+            return acc[name]
+        return acc[name] + act[name][2][:, None] * w[name][0].sum(axis=0)[None, :]
+
+    np.testing.assert_array_equal(planes[0], expect("main", lay.code_centered_main))
+    if "text" in acc:
+        np.testing.assert_array_equal(planes[1], expect("text", lay.code_centered_aux))
+    if "vision" in acc:
+        np.testing.assert_array_equal(planes[2], expect("vision", lay.code_centered_aux))
+    assert planes.shape == (4, T, L.d_out)
+
+
+def _check_out(layer, x, tags, out_dtype=None):
+    pkg = _pkg()
+    L = orc.from_reference_layer(layer)
+    ref = orc.forward(L, x.astype(np.float64), tags)
+    batch = pkg.ActivationBatch(torch.from_numpy(np.ascontiguousarray(x)).cuda(),
+                                torch.from_numpy(tags).cuda())
+    y = pkg.forward(layer, batch, out_dtype=out_dtype).double().cpu().numpy()
+    rms = np.sqrt(np.mean(ref ** 2))
+    if out_dtype in (None, torch.float32):
+        err = np.max(np.abs(y - ref)) / rms
+        assert err <= TOL, f"max err {err:.3e} x rms"
+        return err
+    # half-precision storage: the fp32 result within TOL, then one rounding of
+    # the output type (unit roundoff 2^-11 for fp16, 2^-8 for bf16; F11)
+    u = 2.0 ** -11 if out_dtype == torch.float16 else 2.0 ** -8
+    excess = np.abs(y - ref) - u * np.abs(ref)
+    err = np.max(excess) / rms
+    assert err <= TOL, f"max err beyond output rounding {err:.3e} x rms"
+    return err
+
+
+CASES = {
+    "c1_small": dict(seed=1, T=256, d_in=512, d_out=384, k_t=16, k_v=16, r_s=16, r_c=16),
+    "a8w4": dict(seed=2, T=300, d_in=640, d_out=256, k_t=32, k_v=32, r_s=10, r_c=15, abits=8),
+    "a3w3": dict(seed=3, T=129, d_in=512, d_out=200, k_t=8, k_v=8, r_s=8, r_c=12, abits=3, wbits=3),
+    "a2w3": dict(seed=4, T=77, d_in=384, d_out=144, k_t=8, k_v=8, r_s=4, r_c=6, abits=2, wbits=3),
+    "sym_a4": dict(seed=5, T=200, d_in=512, d_out=256, k_t=16, k_v=16, r_s=8, r_c=8, a_sym=True),
+    "sym_a8": dict(seed=6, T=160, d_in=512, d_out=256, k_t=16, k_v=16, r_s=8, r_c=8, abits=8,
+                   a_sym=True),
+    "no_lowrank": dict(seed=7, T=256, d_in=512, d_out=512, k_t=16, k_v=16, r_s=0, r_c=0),
+    "cws_only": dict(seed=8, T=256, d_in=512, d_out=256, k_t=16, k_v=16, r_s=12, r_c=0),
+    "mac_only": dict(seed=9, T=256, d_in=512, d_out=256, k_t=16, k_v=16, r_s=0, r_c=12),
+    "no_outliers": dict(seed=10, T=256, d_in=512, d_out=256, k_t=0, k_v=0, r_s=8, r_c=8),
+    "all_vision": dict(seed=11, T=200, d_in=512, d_out=256, k_t=16, k_v=16, r_s=8, r_c=8,
+                       n_vision=200),
+    "all_text": dict(seed=12, T=200, d_in=512, d_out=256, k_t=16, k_v=16, r_s=8, r_c=8,
+                     n_vision=0),
+    "one_token": dict(seed=13, T=1, d_in=256, d_out=128, k_t=4, k_v=4, r_s=4, r_c=4, n_vision=0),
+    "k110_down": dict(seed=14, T=300, d_in=2048, d_out=256, k_t=110, k_v=110, r_s=20, r_c=30),
+    "f16_input": dict(seed=15, T=256, d_in=768, d_out=512, k_t=32, k_v=32, r_s=16, r_c=16,
+                      x_dtype=np.float16),
+    "f64_input": dict(seed=16, T=128, d_in=512, d_out=256, k_t=16, k_v=16, r_s=8, r_c=8,
+                      x_dtype=np.float64),
+    "tiny_dout": dict(seed=17, T=64, d_in=128, d_out=12, k_t=4, k_v=4, r_s=2, r_c=3),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_codes_bit_exact(name):
+    layer, x, tags = _case(**CASES[name])
+    _check_codes(layer, x, tags)
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_accumulators_bit_exact(name):
+    layer, x, tags = _case(**CASES[name])
+    _check_acc(layer, x, tags)
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_output_within_tolerance(name):
+    layer, x, tags = _case(**CASES[name])
+    _check_out(layer, x, tags)
+
+
+@pytest.mark.parametrize("dt", ["float16", "bfloat16"])
+def test_half_outputs(dt):
+    layer, x, tags = _case(**CASES["c1_small"])
+    _check_out(layer, x, tags, out_dtype=getattr(torch, dt))
+
+
+def test_config1_full():
+    """BASELINE config 1: codes, accumulators and output vs the oracle."""
+    pkg = _pkg()
+    layer, x, tags = wl.config1(pkg)
+    _check_codes(layer, x, tags)
+    _check_acc(layer, x, tags)
+    err = _check_out(layer, x, tags)
+    assert err < 1e-4
+
+
+def test_numpy_dropin_returns_float64():
+    pkg = _pkg()
+    layer, x, tags = _case(**CASES["c1_small"])
+    batch = pkg.ActivationBatch(x.astype(np.float64), tags)
+    y = pkg.forward(layer, batch)
+    assert isinstance(y, np.ndarray) and y.dtype == np.float64
+    ref = orc.forward(orc.from_reference_layer(layer), x.astype(np.float64), tags)
+    assert np.max(np.abs(y - ref)) <= TOL * np.sqrt(np.mean(ref ** 2))
+
+
+def test_mac_locality_bit_exact():
+    """Vision rows are bit-identical with MAC on vs off (test_layer.py:87-99)."""
+    import dataclasses
+    pkg = _pkg()
+    layer, x, tags = _case(**CASES["c1_small"])
+    off = dataclasses.replace(layer, use_mac=False)
+    xb = torch.from_numpy(x).cuda()
+    tb = torch.from_numpy(tags).cuda()
+    y_on = pkg.forward(layer, pkg.ActivationBatch(xb, tb)).cpu().numpy()
+    y_off = pkg.forward(off, pkg.ActivationBatch(xb, tb)).cpu().numpy()
+    v = tags == 1
+    np.testing.assert_array_equal(y_on[v], y_off[v])
+    assert np.any(y_on[~v] != y_off[~v])
+
+
+def test_data_errors_raise_valueerror():
+    pkg = _pkg()
+    layer, x, tags = _case(**CASES["tiny_dout"])
+    bad = x.copy()
+    bad[3, 5] = np.inf
+    xb = torch.from_numpy(bad).cuda()
+    with pytest.raises(ValueError, match="non-finite"):
+        pkg.forward(layer, pkg.ActivationBatch(xb, torch.from_numpy(tags).cuda()))
+    bad_tags = torch.from_numpy(tags.copy()).cuda()
+    bad_tags[0] = 2
+    with pytest.raises(ValueError, match="tags"):
+        pkg.forward(layer, pkg.ActivationBatch(torch.from_numpy(x).cuda(), bad_tags))
+    with pytest.raises(ValueError, match="width"):
+        pkg.forward(layer, pkg.ActivationBatch(torch.from_numpy(x[:, :-1].copy()).cuda(),
+                                               torch.from_numpy(tags).cuda()))
+
+
+def test_unsupported_specs_raise():
+    import dataclasses
+    pkg = _pkg()
+    layer, x, tags = _case(**CASES["tiny_dout"])
+    for spec in (pkg.QuantSpec(None, False, pkg.Granularity.PER_TOKEN),
+                 pkg.QuantSpec(16, False, pkg.Granularity.PER_TOKEN)):
+        bad = dataclasses.replace(layer, act_spec=spec)
+        with pytest.raises(ValueError):
+            pkg.forward(bad, pkg.ActivationBatch(x.astype(np.float64), tags))
+
+
+def test_quantize_rows_matches_oracle():
+    pkg = _pkg()
+    rng = np.random.default_rng(21)
+    m = rng.standard_normal((37, 1000)) * rng.uniform(0.01, 100, (37, 1))
+    m[5] = 0.7  # constant row
+    m[6] = 0.0  # all-zero row
+    for bits, sym in ((4, False), (8, False), (2, False), (8, True), (3, True)):
+        spec = pkg.QuantSpec(bits, sym, pkg.Granularity.PER_TOKEN)
+        q, p = pkg.quantize_per_token(m, spec)
+        qo, so, zo = orc.codes(m, orc.Spec(bits, sym, orc.PER_TOKEN))
+        np.testing.assert_array_equal(q, qo)
+        np.testing.assert_array_equal(p.scales, so)
+        np.testing.assert_array_equal(p.zero_points, zo)
