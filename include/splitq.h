@@ -59,7 +59,8 @@ extern "C" {
 #define SPLITQ_STATUS_LR_RANGE 8   /* low-rank fp16 operand overflow */
 
 /* forward flags */
-#define SPLITQ_FWD_RAW 1 /* y receives raw accumulators (see splitq_forward) */
+#define SPLITQ_FWD_RAW 1     /* y receives raw accumulators (see splitq_forward) */
+#define SPLITQ_FWD_PROFILE 2 /* record stage events on the stream (splitq_profile_read) */
 
 typedef struct splitq_layer_s* splitq_layer_t;
 
@@ -134,6 +135,11 @@ int splitq_workspace_layout(splitq_layer_t layer, int64_t tokens, splitq_ws_layo
 int splitq_forward(splitq_layer_t layer, const void* x, int x_dtype, int64_t x_ld,
                    const uint8_t* tags, int64_t tokens, void* y, int y_dtype, int64_t y_ld,
                    void* workspace, size_t workspace_bytes, void* stream, int flags);
+
+/* Stage times of the SPLITQ_FWD_PROFILE calls since the last read, summed:
+ * stage_ms[0] = row compaction + K1 quantizer, [1] = low-rank first stages,
+ * [2] = split GEMM. CUDA events on the launch stream; synchronises. */
+int splitq_profile_read(splitq_layer_t layer, double* stage_ms, int32_t* calls);
 
 /* Synchronise `stream` and read the device error word of the workspace;
  * returns SPLITQ_ERR_DATA (with the reference's message) when it is set. */

@@ -21,6 +21,7 @@ SPLITQ_ERR_NCCL = -5
 
 F16, F32, F64, BF16 = 0, 1, 2, 3
 FWD_RAW = 1
+FWD_PROFILE = 2
 
 STATUS_NONFINITE = 1
 STATUS_SCALE = 2
@@ -101,6 +102,7 @@ def load(build_if_missing: bool = True):
         "splitq_forward": (C.c_int, [_p, _p, C.c_int, _i64, _p, _i64, _p, C.c_int, _i64,
                                      _p, C.c_size_t, _p, C.c_int]),
         "splitq_read_status": (C.c_int, [_p, _p, C.POINTER(_i32)]),
+        "splitq_profile_read": (C.c_int, [_p, C.POINTER(C.c_double), C.POINTER(_i32)]),
         "splitq_quantize_rows": (C.c_int, [_p, C.c_int, _i64, _i64, _i64, QSpec, _p, _i64,
                                            _p, _p, _p, C.POINTER(_i32), _p]),
         "splitq_gemm_i8": (C.c_int, [_p, _i64, C.c_int, _p, _i64, _p, _i64, _i64, _i64,
@@ -122,7 +124,7 @@ def load(build_if_missing: bool = True):
 EXPORTED_SYMBOLS = (
     "splitq_last_error", "splitq_version", "splitq_device_sm_count",
     "splitq_layer_create", "splitq_layer_destroy", "splitq_workspace_layout",
-    "splitq_forward", "splitq_read_status", "splitq_quantize_rows", "splitq_gemm_i8",
+    "splitq_forward", "splitq_read_status", "splitq_profile_read", "splitq_quantize_rows", "splitq_gemm_i8",
     "splitq_mocd_absmax", "splitq_mocd_rank_counts", "splitq_mocd_histogram",
     "splitq_mocd_text_score",
 )

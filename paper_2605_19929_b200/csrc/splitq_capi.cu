@@ -148,6 +148,9 @@ struct splitq_layer_s {
   int8_t* b_us = nullptr; float* s_us = nullptr; int* cs_us = nullptr;
   int8_t* b_uc = nullptr; float* s_uc = nullptr; int* cs_uc = nullptr;
   __half* b_lr = nullptr; float* kappa = nullptr;
+  // stage timing (SPLITQ_FWD_PROFILE): 4 events per profiled call
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
 };
 
 namespace {
@@ -357,6 +360,7 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
 int splitq_layer_destroy(splitq_layer_t L) {
   if (!L) return SPLITQ_OK;
   cudaSetDevice(L->device);
+  for (cudaEvent_t e : L->ev_pool) cudaEventDestroy(e);
   L->mem.release();
   delete L;
   return SPLITQ_OK;
@@ -452,6 +456,18 @@ int tile_n(int64_t n) { return (int)std::min<int64_t>(GEMM_MAX_BN, round_up(n, 1
 
 }  // namespace
 
+namespace {
+int prof_record(splitq_layer_s* L, cudaStream_t stream) {
+  if (L->ev_used == L->ev_pool.size()) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    L->ev_pool.push_back(e);
+  }
+  CUDA_TRY(cudaEventRecord(L->ev_pool[L->ev_used++], stream));
+  return SPLITQ_OK;
+}
+}  // namespace
+
 extern "C" {
 
 int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, const uint8_t* tags,
@@ -482,6 +498,8 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   int* text_idx = (int*)at(W.text_idx);
   int* text_rows = (int*)at(W.text_rows);
 
+  const bool prof = (flags & SPLITQ_FWD_PROFILE) != 0;
+  if (prof && (rc = prof_record(L, stream))) return rc;
   CUDA_TRY(cudaMemsetAsync(err, 0, 16, stream));
   compact_text_rows_kernel<<<1, 1024, 0, stream>>>(tags, (int)T, text_idx, text_rows, n_text, err);
   CUDA_TRY(cudaGetLastError());
@@ -530,6 +548,7 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   k.err = err;
   k1_quantize_kernel<<<(unsigned)T, K1_THREADS, 0, stream>>>(k);
   CUDA_TRY(cudaGetLastError());
+  if (prof && (rc = prof_record(L, stream))) return rc;
 
   const uint32_t a_fmt_main = L->act.centered ? 1u : 0u;  // s8 : u8
   const uint32_t a_fmt_aux = L->aux.centered ? 1u : 0u;
@@ -583,6 +602,8 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
     if ((rc = launch_gemm(g, L->device, T, stream))) return rc;
   }
 
+  if (prof && (rc = prof_record(L, stream))) return rc;
+
   // ---- split GEMM: main + outliers + low-rank second stage + merge
   GemmLaunch g{};
   g.p.M = (int)T;
@@ -634,7 +655,27 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
     ok = map_f16(&g.maps.la, lr_a, T, L->k_lr, L->k_lr, GEMM_BM) &&
          map_f16(&g.maps.lb, L->b_lr, L->d_out, L->k_lr, L->k_lr, g.p.bn);
   if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (split GEMM)");
-  return launch_gemm(g, L->device, T, stream);
+  if ((rc = launch_gemm(g, L->device, T, stream))) return rc;
+  if (prof && (rc = prof_record(L, stream))) return rc;
+  return SPLITQ_OK;
+}
+
+int splitq_profile_read(splitq_layer_t L, double* stage_ms, int32_t* calls) {
+  if (!L || !stage_ms) return fail(SPLITQ_ERR_INVALID, "null argument");
+  for (int i = 0; i < 3; ++i) stage_ms[i] = 0.0;
+  const size_t n = L->ev_used / 4;
+  for (size_t c = 0; c < n; ++c) {
+    cudaEvent_t* e = &L->ev_pool[4 * c];
+    CUDA_TRY(cudaEventSynchronize(e[3]));
+    for (int i = 0; i < 3; ++i) {
+      float ms = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&ms, e[i], e[i + 1]));
+      stage_ms[i] += ms;
+    }
+  }
+  if (calls) *calls = (int32_t)n;
+  L->ev_used = 0;
+  return SPLITQ_OK;
 }
 
 int splitq_read_status(void* ws, void* stream_, int32_t* status_out) {

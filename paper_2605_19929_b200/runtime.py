@@ -149,7 +149,8 @@ class GpuLayer:
             self._ws = {tokens: ws}  # keep the latest size only
         return ws
 
-    def run(self, x, tags, y=None, out_dtype=None, raw=False, check=True, ws=None):
+    def run(self, x, tags, y=None, out_dtype=None, raw=False, check=True, ws=None,
+            profile=False):
         """Launch the forward on the current stream. x: CUDA [T x >=d_in]
         (f16/bf16/f32/f64, unit column stride), tags: CUDA uint8 [T]."""
         torch = _torch()
@@ -173,11 +174,21 @@ class GpuLayer:
         y_ld = y.stride(-2)
         _lib.check(lib.splitq_forward(self.handle, _ptr(x), _dtype_code(x.dtype), x.stride(0),
                                       _ptr(tags), T, _ptr(y), ydt, y_ld, _ptr(ws),
-                                      ws.numel(), _stream(), _lib.FWD_RAW if raw else 0))
+                                      ws.numel(), _stream(),
+                                      (_lib.FWD_RAW if raw else 0) | (_lib.FWD_PROFILE if profile else 0)))
         if check:
             st = C.c_int32()
             _lib.check(lib.splitq_read_status(_ptr(ws), _stream(), C.byref(st)))
         return y
+
+
+    def profile_read(self):
+        """Summed stage times (ms) of the profiled calls since the last read:
+        (quantize, low-rank first stages, split GEMM), number of calls."""
+        ms = (C.c_double * 3)()
+        calls = C.c_int32()
+        _lib.check(_lib.load().splitq_profile_read(self.handle, ms, C.byref(calls)))
+        return list(ms), calls.value
 
 
 _PACKED: dict = {}
