@@ -1,0 +1,418 @@
+// K1 (throughput version): fused gather / smoothing / per-token quantization
+// and MAC residual codes, one CTA per block of rows.
+//
+// Same exactness contract as quantize.cuh (reference quantizer.py:104-155,
+// transform.py:94-103, layer.py:135-136 / 157-160), restructured for HBM
+// speed on sm_100a:
+//   * the x row is staged in SMEM with double-buffered 16-B cp.async, so the
+//     gather x[c_main[k]] is an SMEM read and HBM is read exactly once;
+//   * z = x * d (fp64) stays in registers (EPT per thread) across the
+//     min/max pass, the code pass and the MAC residual pass;
+//   * rounding: v = z * (1/S) and RNE(|v|) via the 1.5*2^52 magic constant
+//     (5 fp64 ops); within 1e-6 of a .5 tie the exact reference expression
+//     floor(fl(|z / S| + 0.5)) is evaluated instead, so codes are identical;
+//   * x_hat = (q - zp) * S comes from a per-row table of the <= 256 code
+//     levels (one fp64 product per level, the reference's rounding).
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "quantize.cuh"
+
+namespace splitq {
+
+constexpr double K1_MAGIC = 6755399441055744.0;  // 1.5 * 2^52
+
+template <typename T>
+__device__ __forceinline__ double to_f64(T v);
+template <>
+__device__ __forceinline__ double to_f64<__half>(__half v) { return (double)__half2float(v); }
+template <>
+__device__ __forceinline__ double to_f64<__nv_bfloat16>(__nv_bfloat16 v) {
+  return (double)__bfloat162float(v);
+}
+template <>
+__device__ __forceinline__ double to_f64<float>(float v) { return (double)v; }
+template <>
+__device__ __forceinline__ double to_f64<double>(double v) { return v; }
+
+template <typename T>
+__device__ __forceinline__ bool finite_in(T v) {
+  return isfinite(to_f64(v));
+}
+
+// q = clip(rha(m / S) + zp, qmin, qmax) with the reference's rounding
+// (quantizer.py:76-77, 152-154); rS = 1 / S.
+__device__ __forceinline__ int quant_fast(double m, double S, double rS, int zp, int qmin,
+                                          int qmax) {
+  const double v = __dmul_rn(m, rS);
+  const double a = fabs(v);
+  int n;
+  if (__double2hiint(a) >= 0x41D00000) {  // |v| >= 2^30: saturates after clipping
+    n = 1 << 30;
+  } else {
+    const double t = __dadd_rn(a, K1_MAGIC);
+    const double diff = __dsub_rn(a, __dsub_rn(t, K1_MAGIC));  // a - RNE(a), in [-0.5, 0.5]
+    n = __double2loint(t);
+    if (diff > 0.499999 || diff < -0.499999) {  // near a tie: exact reference expression
+      const double ve = __ddiv_rn(m, S);
+      n = (int)floor(__dadd_rn(fabs(ve), 0.5));
+      return min(max((ve < 0.0 ? -n : n) + zp, qmin), qmax);
+    }
+  }
+  const int q = (__double2hiint(v) < 0 ? -n : n) + zp;
+  return min(max(q, qmin), qmax);
+}
+
+struct K1Smem {
+  // per-warp partial min / max of the current reduction
+  double red_lo[32], red_hi[32];
+  double red2_lo[32], red2_hi[32];
+  double xh[256];  // x_hat of every code level of the current row
+  int bad[2];      // per row parity: a non-finite x was seen
+};
+
+template <int EPT>
+struct K1Bounds {
+  static constexpr int max_threads = 512;         // host keeps NT <= 512
+  static constexpr bool cache_tables = EPT <= 8;  // gather table held in registers
+};
+
+__device__ __forceinline__ void reduce_minmax(double& lo, double& hi, double* slo, double* shi) {
+  const int NW = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    slo[warp] = lo;
+    shi[warp] = hi;
+  }
+  __syncthreads();
+  lo = slo[0];
+  hi = shi[0];
+  for (int w = 1; w < NW; ++w) {
+    lo = fmin(lo, slo[w]);
+    hi = fmax(hi, shi[w]);
+  }
+}
+
+// Copy one x row (n elements of T) into SMEM with 16-B cp.async when aligned.
+template <typename T>
+__device__ __forceinline__ void stage_row_async(T* dst, const T* src, int n, bool aligned16) {
+  if (aligned16) {
+    const int nvec = (n * (int)sizeof(T)) / 16;
+    const char* s = reinterpret_cast<const char*>(src);
+    char* d = reinterpret_cast<char*>(dst);
+    for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(d + 16 * i)),
+                   "l"(s + 16 * i)
+                   : "memory");
+    }
+    for (int i = nvec * 16 / (int)sizeof(T) + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// Outlier path of one row by one warp, reading x from SMEM.
+template <typename T>
+__device__ void outlier_row_smem(const K1Params& p, int row, const T* xs, const int* cols,
+                                 const double* d, int n, int ld, int8_t* codes, double* s_out,
+                                 float* sf_out, int* zp_out) {
+  const int lane = threadIdx.x & 31;
+  double lo = INFINITY, hi = -INFINITY;
+  for (int k = lane; k < n; k += 32) {
+    const double z = __dmul_rn(to_f64(xs[cols[k]]), d[k]);
+    lo = fmin(lo, z);
+    hi = fmax(hi, z);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if (!isfinite(lo) || !isfinite(hi)) {
+    if (lane == 0) atomicOr(p.err, ERR_NONFINITE);
+    return;
+  }
+  double S, zpd;
+  if (!group_params(lo, hi, p.aux, &S, &zpd)) {
+    if (lane == 0) atomicOr(p.err, ERR_SCALE_ZERO);
+    S = 1.0;
+  }
+  const double rS = __ddiv_rn(1.0, S);
+  const int zp = (int)zpd;
+  int8_t* out = codes + (int64_t)row * ld;
+  for (int k = lane; k < ld; k += 32) {
+    int8_t c = 0;
+    if (k < n) {
+      const double z = __dmul_rn(to_f64(xs[cols[k]]), d[k]);
+      const int q = quant_fast(z, S, rS, zp, p.aux.qmin, p.aux.qmax);
+      c = p.aux.centered ? (int8_t)(q - zp) : (int8_t)(uint8_t)q;
+    }
+    out[k] = c;
+  }
+  if (lane == 0) {
+    s_out[row] = S;
+    sf_out[row] = (float)S;
+    zp_out[row] = zp;
+  }
+}
+
+// Exact-path fallback for quant_fast, kept out of line so the unrolled
+// element loops stay small.
+__device__ __noinline__ int quant_exact(double m, double S, double zp_qmin_qmax_packed_unused,
+                                        int zp, int qmin, int qmax) {
+  const double ve = __ddiv_rn(m, S);
+  const int n = (int)floor(__dadd_rn(fabs(ve), 0.5));
+  return min(max((ve < 0.0 ? -n : n) + zp, qmin), qmax);
+}
+
+// quant_fast without the inline slow path; see quant_fast for the contract.
+__device__ __forceinline__ int quant_lean(double m, double S, double rS, int zp, int qmin,
+                                          int qmax) {
+  const double v = __dmul_rn(m, rS);
+  const double a = fabs(v);
+  const double t = __dadd_rn(a, K1_MAGIC);
+  const double diff = __dsub_rn(a, __dsub_rn(t, K1_MAGIC));  // a - RNE(a)
+  int n = __double2loint(t);
+  // |v| >= 2^30 saturates after clipping; |diff| near 0.5 is a potential tie
+  if (__double2hiint(a) >= 0x41D00000) n = 1 << 30;
+  else if (fabs(diff) > 0.499999) return quant_exact(m, S, 0.0, zp, qmin, qmax);
+  const int q = (__double2hiint(v) < 0 ? -n : n) + zp;
+  return min(max(q, qmin), qmax);
+}
+
+__device__ __forceinline__ void minmax_upd(double z, double& lo, double& hi) {
+  lo = z < lo ? z : lo;  // NaN never enters (checked separately)
+  hi = z > hi ? z : hi;
+}
+
+__device__ __forceinline__ void warp_minmax(double& lo, double& hi) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+    const double h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = l2 < lo ? l2 : lo;
+    hi = h2 > hi ? h2 : hi;
+  }
+}
+
+// Gather 4 main elements k0..k0+3 of one row: z = x[c_main[k]] * d_main[k].
+// `full` = all four inside n_main (vector table loads); lanes outside get z = 0.
+template <typename T, bool GATHER>
+__device__ __forceinline__ void gather4(const K1Params& p, const T* xrow, int k0, bool full,
+                                        double (&z)[4]) {
+  if (full) {
+    int c[4];
+    double d[4];
+    if (GATHER) {
+      const int4 c4 = __ldg(reinterpret_cast<const int4*>(p.c_main + k0));
+      c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
+      const double2 d0 = __ldg(reinterpret_cast<const double2*>(p.d_main + k0));
+      const double2 d1 = __ldg(reinterpret_cast<const double2*>(p.d_main + k0 + 2));
+      d[0] = d0.x; d[1] = d0.y; d[2] = d1.x; d[3] = d1.y;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double xv = to_f64(__ldg(xrow + (GATHER ? c[u] : k0 + u)));
+      z[u] = GATHER ? __dmul_rn(xv, d[u]) : xv;
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + u;
+      z[u] = 0.0;
+      if (k < p.n_main) {
+        const double xv = to_f64(__ldg(xrow + (GATHER ? __ldg(p.c_main + k) : k)));
+        z[u] = GATHER ? __dmul_rn(xv, __ldg(p.d_main + k)) : xv;
+      }
+    }
+  }
+}
+
+// Outlier path of one row by one warp (x read through L1).
+template <typename T>
+__device__ void outlier_row_warp(const K1Params& p, int row, const T* xrow, const int* cols,
+                                 const double* d, int n, int ld, int8_t* codes, double* s_out,
+                                 float* sf_out, int* zp_out) {
+  const int lane = threadIdx.x & 31;
+  double lo = INFINITY, hi = -INFINITY;
+  bool nan = false;
+  for (int k = lane; k < n; k += 32) {
+    const double z = __dmul_rn(to_f64(__ldg(xrow + cols[k])), d[k]);
+    nan |= z != z;
+    lo = z < lo ? z : lo;
+    hi = z > hi ? z : hi;
+  }
+  warp_minmax(lo, hi);
+  if (__any_sync(0xffffffffu, nan) || !isfinite(lo) || !isfinite(hi)) {
+    if (lane == 0) atomicOr(p.err, ERR_NONFINITE);
+    return;
+  }
+  double S, zpd;
+  const bool ok = group_params(lo, hi, p.aux, &S, &zpd);
+  if (!ok) S = 1.0;
+  const double rS = __ddiv_rn(1.0, S);
+  const int zp = (int)zpd;
+  int8_t* out = codes + (int64_t)row * ld;
+  for (int k = lane; k < ld; k += 32) {
+    int c = 0;
+    if (k < n) {
+      const double z = __dmul_rn(to_f64(__ldg(xrow + cols[k])), d[k]);
+      const int q = quant_lean(z, S, rS, zp, p.aux.qmin, p.aux.qmax);
+      c = p.aux.centered ? q - zp : q;
+    }
+    out[k] = (int8_t)c;
+  }
+  if (lane == 0) {
+    if (!ok) atomicOr(p.err, ERR_SCALE_ZERO);
+    s_out[row] = S;
+    sf_out[row] = (float)S;
+    zp_out[row] = zp;
+  }
+}
+
+constexpr int K1W_WARPS = 8;
+
+// One warp per token row; reductions are warp shuffles only, so dozens of
+// rows are in flight per SM and the per-row parameter chain is hidden.
+// x is read from global (first pass from HBM, re-reads hit L1 / L2).
+template <typename T, bool GATHER>
+__global__ void __launch_bounds__(K1W_WARPS * 32) k1_warp_kernel(const K1Params p) {
+  __shared__ double xh_all[K1W_WARPS][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * K1W_WARPS + warp;
+  if (row >= p.T) return;
+  double* xh = xh_all[warp];
+  const T* xrow = reinterpret_cast<const T*>(p.x) + (int64_t)row * p.ldx;
+  const int n_main = p.n_main, ld = p.ld_main;
+  const int qmin = p.act.qmin, qmax = p.act.qmax;
+
+  // ---- pass 1: row min / max of z = x * d
+  double lo = INFINITY, hi = -INFINITY;
+  bool nan = false;
+  for (int k0 = 4 * lane; k0 < n_main; k0 += 128) {
+    double z[4];
+    gather4<T, GATHER>(p, xrow, k0, k0 + 3 < n_main, z);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      nan |= z[u] != z[u];
+      if (k0 + u < n_main) {
+        lo = z[u] < lo ? z[u] : lo;
+        hi = z[u] > hi ? z[u] : hi;
+      }
+    }
+  }
+  warp_minmax(lo, hi);
+  if (__any_sync(0xffffffffu, nan) || !isfinite(lo) || !isfinite(hi)) {
+    if (lane == 0) atomicOr(p.err, ERR_NONFINITE);
+    return;
+  }
+  double S, zpd;
+  const bool ok = group_params(lo, hi, p.act, &S, &zpd);  // identical in every lane
+  if (!ok) S = 1.0;
+  const double rS = __ddiv_rn(1.0, S);
+  const int zp = (int)zpd;
+  const int cix = p.use_mac ? p.text_idx[row] : -1;
+  const bool mac = cix >= 0;
+  const bool cen = p.act.centered != 0;
+  if (lane == 0) {
+    if (!ok) atomicOr(p.err, ERR_SCALE_ZERO);
+    p.s_main[row] = S;
+    if (p.sf_main) p.sf_main[row] = (float)S;
+    p.zp_main[row] = zp;
+    if (p.rho) {
+      int e;
+      frexp(S, &e);
+      const double rho = ldexp(1.0, e - 1);
+      p.rho[row] = (float)rho;
+      p.lrs_main[row] = (float)(S / rho);
+    }
+  }
+  if (mac) {
+    for (int n = lane; n <= qmax - qmin; n += 32)
+      xh[n] = __dmul_rn((double)(n + qmin - zp), S);  // fake_quantize's (q - z) * S
+    __syncwarp();
+  }
+
+  // ---- pass 2: main codes, 4 per 32-bit store; MAC residual range
+  int8_t* arow = p.a_main + (int64_t)row * ld;
+  double elo = INFINITY, ehi = -INFINITY;
+  for (int k0 = 4 * lane; k0 < ld; k0 += 128) {
+    double z[4];
+    gather4<T, GATHER>(p, xrow, k0, k0 + 3 < n_main, z);
+    uint32_t packed = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool in = k0 + u < n_main;
+      const int q = quant_lean(z[u], S, rS, zp, qmin, qmax);
+      packed |= (uint32_t)((in ? (cen ? q - zp : q) : 0) & 0xFF) << (8 * u);
+      if (mac && in) {
+        const double e = __dsub_rn(z[u], xh[q - qmin]);
+        elo = e < elo ? e : elo;
+        ehi = e > ehi ? e : ehi;
+      }
+    }
+    *reinterpret_cast<uint32_t*>(arow + k0) = packed;
+  }
+
+  // ---- outlier paths and the low-rank operand row clear (same warp)
+  if (p.n_text > 0)
+    outlier_row_warp(p, row, xrow, p.c_text, p.d_text, p.n_text, p.ld_text, p.a_text, p.s_text,
+                     p.sf_text, p.zp_text);
+  if (p.n_vis > 0)
+    outlier_row_warp(p, row, xrow, p.c_vis, p.d_vis, p.n_vis, p.ld_vis, p.a_vis, p.s_vis,
+                     p.sf_vis, p.zp_vis);
+  if (p.k_lr > 0) {
+    uint4* lr = reinterpret_cast<uint4*>(p.lr_a + (int64_t)row * p.k_lr);
+    for (int i = lane; i < p.k_lr / 8; i += 32) lr[i] = make_uint4(0, 0, 0, 0);
+  }
+  if (!mac) return;
+
+  // ---- pass 3 (text rows): residual codes at the aux width (layer.py:159-160);
+  // q is read back from this warp's own code row (same lanes, program order)
+  warp_minmax(elo, ehi);
+  double Se, zped;
+  const bool oke = group_params(elo, ehi, p.aux, &Se, &zped);
+  if (!oke) Se = 1.0;
+  const double rSe = __ddiv_rn(1.0, Se);
+  const int zpe = (int)zped;
+  const bool cena = p.aux.centered != 0;
+  if (lane == 0) {
+    if (!oke) atomicOr(p.err, ERR_SCALE_ZERO);
+    p.s_mac[cix] = Se;
+    p.zp_mac[cix] = zpe;
+    int e;
+    frexp(S, &e);
+    p.lrs_mac[cix] = (float)(Se / ldexp(1.0, e - 1));
+  }
+  int8_t* erow = p.a_mac + (int64_t)cix * ld;
+  for (int k0 = 4 * lane; k0 < ld; k0 += 128) {
+    double z[4];
+    gather4<T, GATHER>(p, xrow, k0, k0 + 3 < n_main, z);
+    const uint32_t codes = *reinterpret_cast<const uint32_t*>(arow + k0);
+    uint32_t packed = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = cen ? (int)(int8_t)(codes >> (8 * u)) : (int)((codes >> (8 * u)) & 0xFF);
+      const int q = cen ? c + zp : c;
+      const double e = __dsub_rn(z[u], xh[q - qmin]);
+      const int qe = quant_lean(e, Se, rSe, zpe, p.aux.qmin, p.aux.qmax);
+      const bool in = k0 + u < n_main;
+      packed |= (uint32_t)((in ? (cena ? qe - zpe : qe) : 0) & 0xFF) << (8 * u);
+    }
+    *reinterpret_cast<uint32_t*>(erow + k0) = packed;
+  }
+}
+
+}  // namespace splitq

@@ -16,6 +16,7 @@
 #include "../../include/splitq.h"
 #include "gemm_sm100.cuh"
 #include "quantize.cuh"
+#include "quantize_fast.cuh"
 #include "tma_host.cuh"
 
 using namespace splitq;
@@ -456,6 +457,43 @@ int tile_n(int64_t n) { return (int)std::min<int64_t>(GEMM_MAX_BN, round_up(n, 1
 
 }  // namespace
 
+
+namespace {
+
+template <typename T, bool G>
+int launch_k1_t(const K1Params& k, cudaStream_t stream) {
+  const unsigned grid = (unsigned)((k.T + K1W_WARPS - 1) / K1W_WARPS);
+  k1_warp_kernel<T, G><<<grid, K1W_WARPS * 32, 0, stream>>>(k);
+  CUDA_TRY(cudaGetLastError());
+  return SPLITQ_OK;
+}
+
+template <bool G>
+int launch_k1_dt(const K1Params& k, cudaStream_t s) {
+  switch (k.x_dtype) {
+    case IN_F16: return launch_k1_t<__half, G>(k, s);
+    case IN_BF16: return launch_k1_t<__nv_bfloat16, G>(k, s);
+    case IN_F32: return launch_k1_t<float, G>(k, s);
+    default: return launch_k1_t<double, G>(k, s);
+  }
+}
+
+// K1 dispatch: warp-per-row kernel (generic per-row CTA kernel kept for code
+// matrices whose row stride is not a multiple of 16 bytes).
+int launch_k1(const K1Params& k, int d_in, int device, cudaStream_t stream) {
+  (void)d_in;
+  (void)device;
+  if (k.ld_main & 15) {
+    k1_quantize_kernel<<<(unsigned)k.T, K1_THREADS, 0, stream>>>(k);
+    CUDA_TRY(cudaGetLastError());
+    return SPLITQ_OK;
+  }
+  if (k.c_main && k.d_main) return launch_k1_dt<true>(k, stream);
+  return launch_k1_dt<false>(k, stream);
+}
+
+}  // namespace
+
 namespace {
 int prof_record(splitq_layer_s* L, cudaStream_t stream) {
   if (L->ev_used == L->ev_pool.size()) {
@@ -546,8 +584,7 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   k.lr_a = (__half*)at(W.lr_a);
   k.k_lr = (int)L->k_lr;
   k.err = err;
-  k1_quantize_kernel<<<(unsigned)T, K1_THREADS, 0, stream>>>(k);
-  CUDA_TRY(cudaGetLastError());
+  if ((rc = launch_k1(k, (int)L->d_in, L->device, stream))) return rc;
   if (prof && (rc = prof_record(L, stream))) return rc;
 
   const uint32_t a_fmt_main = L->act.centered ? 1u : 0u;  // s8 : u8
@@ -720,9 +757,9 @@ int splitq_quantize_rows(const void* x, int x_dtype, int64_t x_ld, int64_t rows,
   k.s_main = scales;
   k.zp_main = zero_points;
   k.err = status;
-  k1_quantize_kernel<<<(unsigned)rows, K1_THREADS, 0, stream>>>(k);
-  CUDA_TRY(cudaGetLastError());
-  return SPLITQ_OK;
+  int device = 0;
+  CUDA_TRY(cudaGetDevice(&device));
+  return launch_k1(k, (int)cols, device, stream);
 }
 
 int splitq_gemm_i8(const int8_t* a, int64_t lda, int a_signed, const int8_t* b, int64_t ldb,
