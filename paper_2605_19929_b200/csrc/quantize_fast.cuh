@@ -282,28 +282,203 @@ __device__ void outlier_row_warp(const K1Params& p, int row, const T* xrow, cons
   }
 }
 
-constexpr int K1W_WARPS = 8;
+constexpr int K1G_WARPS = 8;  // warps per CTA; a row group is G of them
 
-// One warp per token row; reductions are warp shuffles only, so dozens of
-// rows are in flight per SM and the per-row parameter chain is hidden.
-// x is read from global (first pass from HBM, re-reads hit L1 / L2).
+// Round-to-nearest code with the zero point folded into the magic constant:
+// t = v + (1.5 * 2^52 + zp) puts RN(v) + zp in the low word. Outside a 1e-6
+// window around .5 ties RN equals the reference's half-away rounding
+// (quantizer.py:76-77); inside it `tie` is set and the caller re-evaluates
+// exactly. Valid for |v| < 2^29 (the caller guarantees it per row).
+__device__ __forceinline__ int quant_rn(double m, double rS, double cz, bool& tie) {
+  const double v = __dmul_rn(m, rS);
+  const double t = __dadd_rn(v, cz);
+  const double r = __dsub_rn(t, cz);  // RN(v), exact
+  tie |= fabs(__dsub_rn(v, r)) > 0.499999;
+  return __double2loint(t);
+}
+
+struct RowParams {
+  double S, rS, cz;
+  int zp, qmin, qmax;
+  bool safe;  // |z / S| < 2^29 over the row: quant_rn is valid
+};
+
+__device__ __forceinline__ RowParams make_row_params(double lo, double hi, const QSpecDev& s,
+                                                     bool* ok) {
+  RowParams r;
+  double zpd;
+  *ok = group_params(lo, hi, s, &r.S, &zpd);
+  if (!*ok) r.S = 1.0;
+  r.rS = __ddiv_rn(1.0, r.S);
+  r.zp = (int)zpd;
+  r.cz = K1_MAGIC + zpd;
+  r.qmin = s.qmin;
+  r.qmax = s.qmax;
+  r.safe = fmax(fabs(lo), fabs(hi)) * r.rS < 536870912.0;  // 2^29
+  return r;
+}
+
+__device__ __forceinline__ int quant_row(double m, const RowParams& r, bool& tie) {
+  int q;
+  if (r.safe) {
+    q = quant_rn(m, r.rS, r.cz, tie);
+  } else {  // exact reference expression (rows with a huge offset relative to their span)
+    q = quant_exact(m, r.S, 0.0, r.zp, r.qmin, r.qmax);
+  }
+  return min(max(q, r.qmin), r.qmax);
+}
+
+template <int G>
+__device__ __forceinline__ void group_sync(int g) {
+  if (G == 1) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(32 * G) : "memory");
+  }
+}
+
+// min / max over the row group (warp shuffles, then SMEM across its warps)
+template <int G>
+__device__ __forceinline__ void group_minmax(double& lo, double& hi, double* red, int g, int wg) {
+  warp_minmax(lo, hi);
+  if (G > 1) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) {
+      red[2 * wg] = lo;
+      red[2 * wg + 1] = hi;
+    }
+    group_sync<G>(g);
+#pragma unroll
+    for (int w = 0; w < G; ++w) {
+      const double l2 = red[2 * w], h2 = red[2 * w + 1];
+      lo = l2 < lo ? l2 : lo;
+      hi = h2 > hi ? h2 : hi;
+    }
+    group_sync<G>(g);  // red is reused by the next reduction
+  }
+}
+
 template <typename T, bool GATHER>
-__global__ void __launch_bounds__(K1W_WARPS * 32) k1_warp_kernel(const K1Params p) {
-  __shared__ double xh_all[K1W_WARPS][256];
+__device__ __forceinline__ void gather4_smem(const K1Params& p, const T* xs, int k0, bool full,
+                                             double (&z)[4]) {
+  if (full) {
+    int c[4];
+    double d[4];
+    if (GATHER) {
+      const int4 c4 = __ldg(reinterpret_cast<const int4*>(p.c_main + k0));
+      c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
+      const double2 d0 = __ldg(reinterpret_cast<const double2*>(p.d_main + k0));
+      const double2 d1 = __ldg(reinterpret_cast<const double2*>(p.d_main + k0 + 2));
+      d[0] = d0.x; d[1] = d0.y; d[2] = d1.x; d[3] = d1.y;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double xv = to_f64(xs[GATHER ? c[u] : k0 + u]);
+      z[u] = GATHER ? __dmul_rn(xv, d[u]) : xv;
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + u;
+      z[u] = 0.0;
+      if (k < p.n_main) {
+        const double xv = to_f64(xs[GATHER ? __ldg(p.c_main + k) : k]);
+        z[u] = GATHER ? __dmul_rn(xv, __ldg(p.d_main + k)) : xv;
+      }
+    }
+  }
+}
+
+// Outlier path of one row by one warp, x from the staged SMEM row.
+template <typename T>
+__device__ void outlier_row_sm(const K1Params& p, int row, const T* xs, const int* cols,
+                               const double* d, int n, int ld, int8_t* codes, double* s_out,
+                               float* sf_out, int* zp_out) {
+  const int lane = threadIdx.x & 31;
+  double lo = INFINITY, hi = -INFINITY;
+  bool nan = false;
+  for (int k = lane; k < n; k += 32) {
+    const double z = __dmul_rn(to_f64(xs[cols[k]]), d[k]);
+    nan |= z != z;
+    lo = z < lo ? z : lo;
+    hi = z > hi ? z : hi;
+  }
+  warp_minmax(lo, hi);
+  if (__any_sync(0xffffffffu, nan) || !isfinite(lo) || !isfinite(hi)) {
+    if (lane == 0) atomicOr(p.err, ERR_NONFINITE);
+    return;
+  }
+  bool ok;
+  const RowParams rp = make_row_params(lo, hi, p.aux, &ok);
+  int8_t* out = codes + (int64_t)row * ld;
+  for (int k = lane; k < ld; k += 32) {
+    int c = 0;
+    if (k < n) {
+      const double z = __dmul_rn(to_f64(xs[cols[k]]), d[k]);
+      bool tie = false;
+      int q = quant_row(z, rp, tie);
+      if (tie) q = quant_exact(z, rp.S, 0.0, rp.zp, rp.qmin, rp.qmax);
+      c = p.aux.centered ? q - rp.zp : q;
+    }
+    out[k] = (int8_t)c;
+  }
+  if (lane == 0) {
+    if (!ok) atomicOr(p.err, ERR_SCALE_ZERO);
+    s_out[row] = rp.S;
+    sf_out[row] = (float)rp.S;
+    zp_out[row] = rp.zp;
+  }
+}
+
+// One row per group of G warps (K1G_WARPS / G rows per CTA). The row is
+// staged into SMEM with one TMA bulk copy (cp.async.bulk) when it is 16-B
+// aligned, then every pass gathers from SMEM.
+template <typename T, bool GATHER, int G>
+__global__ void __launch_bounds__(K1G_WARPS * 32) k1_group_kernel(const K1Params p, int d_in) {
+  constexpr int NG = K1G_WARPS / G;  // row groups per CTA
+  extern __shared__ __align__(128) uint8_t k1g_smem[];
+  const int row_bytes = (d_in * (int)sizeof(T) + 127) / 128 * 128;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row = blockIdx.x * K1W_WARPS + warp;
-  if (row >= p.T) return;
-  double* xh = xh_all[warp];
+  const int g = warp / G, wg = warp % G;  // group, warp within group
+  const int tg = wg * 32 + lane;          // thread within group
+  constexpr int NTG = 32 * G;
+  uint8_t* base = k1g_smem + g * (row_bytes + 256 * 8 + 2 * G * 8 + 64);
+  T* xs = reinterpret_cast<T*>(base);
+  double* xh = reinterpret_cast<double*>(base + row_bytes);
+  double* red = xh + 256;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(red + 2 * G);
+  const int row = blockIdx.x * NG + g;
+  if (row >= p.T) return;  // whole group exits together
   const T* xrow = reinterpret_cast<const T*>(p.x) + (int64_t)row * p.ldx;
   const int n_main = p.n_main, ld = p.ld_main;
-  const int qmin = p.act.qmin, qmax = p.act.qmax;
+
+  // ---- stage the row
+  const uint32_t bytes = (uint32_t)(d_in * sizeof(T));
+  const bool bulk = (bytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(xrow) & 15) == 0);
+  if (bulk) {
+    if (tg == 0) {
+      mbar_init(mbar, 1);
+      fence_mbar_init();
+      mbar_arrive_expect_tx(mbar, bytes);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+              "r"(smem_u32(xs)),
+          "l"(xrow), "r"(bytes), "r"(smem_u32(mbar))
+          : "memory");
+    }
+    group_sync<G>(g);  // barrier initialised before anyone waits on it
+    mbar_wait(mbar, 0);
+  } else {
+    for (int i = tg; i < d_in; i += NTG) xs[i] = xrow[i];
+    group_sync<G>(g);
+  }
 
   // ---- pass 1: row min / max of z = x * d
   double lo = INFINITY, hi = -INFINITY;
   bool nan = false;
-  for (int k0 = 4 * lane; k0 < n_main; k0 += 128) {
+  for (int k0 = 4 * tg; k0 < n_main; k0 += 4 * NTG) {
     double z[4];
-    gather4<T, GATHER>(p, xrow, k0, k0 + 3 < n_main, z);
+    gather4_smem<T, GATHER>(p, xs, k0, k0 + 3 < n_main, z);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       nan |= z[u] != z[u];
@@ -313,52 +488,65 @@ __global__ void __launch_bounds__(K1W_WARPS * 32) k1_warp_kernel(const K1Params 
       }
     }
   }
-  warp_minmax(lo, hi);
-  if (__any_sync(0xffffffffu, nan) || !isfinite(lo) || !isfinite(hi)) {
-    if (lane == 0) atomicOr(p.err, ERR_NONFINITE);
+  nan = __any_sync(0xffffffffu, nan);
+  if (G > 1) {
+    if (lane == 0) red[2 * wg] = nan ? 1.0 : 0.0;
+    group_sync<G>(g);
+    double any = 0.0;
+    for (int w = 0; w < G; ++w) any += red[2 * w];
+    nan = any != 0.0;
+    group_sync<G>(g);
+  }
+  group_minmax<G>(lo, hi, red, g, wg);
+  if (nan || !isfinite(lo) || !isfinite(hi)) {  // group-uniform
+    if (tg == 0) atomicOr(p.err, ERR_NONFINITE);
     return;
   }
-  double S, zpd;
-  const bool ok = group_params(lo, hi, p.act, &S, &zpd);  // identical in every lane
-  if (!ok) S = 1.0;
-  const double rS = __ddiv_rn(1.0, S);
-  const int zp = (int)zpd;
+  bool ok;
+  const RowParams rp = make_row_params(lo, hi, p.act, &ok);  // identical in every thread
   const int cix = p.use_mac ? p.text_idx[row] : -1;
   const bool mac = cix >= 0;
   const bool cen = p.act.centered != 0;
-  if (lane == 0) {
+  if (tg == 0) {
     if (!ok) atomicOr(p.err, ERR_SCALE_ZERO);
-    p.s_main[row] = S;
-    if (p.sf_main) p.sf_main[row] = (float)S;
-    p.zp_main[row] = zp;
+    p.s_main[row] = rp.S;
+    if (p.sf_main) p.sf_main[row] = (float)rp.S;
+    p.zp_main[row] = rp.zp;
     if (p.rho) {
       int e;
-      frexp(S, &e);
+      frexp(rp.S, &e);
       const double rho = ldexp(1.0, e - 1);
       p.rho[row] = (float)rho;
-      p.lrs_main[row] = (float)(S / rho);
+      p.lrs_main[row] = (float)(rp.S / rho);
     }
   }
   if (mac) {
-    for (int n = lane; n <= qmax - qmin; n += 32)
-      xh[n] = __dmul_rn((double)(n + qmin - zp), S);  // fake_quantize's (q - z) * S
-    __syncwarp();
+    for (int n = tg; n <= rp.qmax - rp.qmin; n += NTG)
+      xh[n] = __dmul_rn((double)(n + rp.qmin - rp.zp), rp.S);  // fake_quantize's (q - z) * S
+    group_sync<G>(g);
   }
 
-  // ---- pass 2: main codes, 4 per 32-bit store; MAC residual range
+  // ---- pass 2: main codes (4 per 32-bit store) + MAC residual range
   int8_t* arow = p.a_main + (int64_t)row * ld;
   double elo = INFINITY, ehi = -INFINITY;
-  for (int k0 = 4 * lane; k0 < ld; k0 += 128) {
+  for (int k0 = 4 * tg; k0 < ld; k0 += 4 * NTG) {
     double z[4];
-    gather4<T, GATHER>(p, xrow, k0, k0 + 3 < n_main, z);
+    gather4_smem<T, GATHER>(p, xs, k0, k0 + 3 < n_main, z);
+    int q[4];
+    bool tie = false;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) q[u] = quant_row(z[u], rp, tie);
+    if (tie) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q[u] = quant_exact(z[u], rp.S, 0.0, rp.zp, rp.qmin, rp.qmax);
+    }
     uint32_t packed = 0;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const bool in = k0 + u < n_main;
-      const int q = quant_lean(z[u], S, rS, zp, qmin, qmax);
-      packed |= (uint32_t)((in ? (cen ? q - zp : q) : 0) & 0xFF) << (8 * u);
+      packed |= (uint32_t)((in ? (cen ? q[u] - rp.zp : q[u]) : 0) & 0xFF) << (8 * u);
       if (mac && in) {
-        const double e = __dsub_rn(z[u], xh[q - qmin]);
+        const double e = __dsub_rn(z[u], xh[q[u] - rp.qmin]);
         elo = e < elo ? e : elo;
         ehi = e > ehi ? e : ehi;
       }
@@ -366,53 +554,65 @@ __global__ void __launch_bounds__(K1W_WARPS * 32) k1_warp_kernel(const K1Params 
     *reinterpret_cast<uint32_t*>(arow + k0) = packed;
   }
 
-  // ---- outlier paths and the low-rank operand row clear (same warp)
-  if (p.n_text > 0)
-    outlier_row_warp(p, row, xrow, p.c_text, p.d_text, p.n_text, p.ld_text, p.a_text, p.s_text,
-                     p.sf_text, p.zp_text);
-  if (p.n_vis > 0)
-    outlier_row_warp(p, row, xrow, p.c_vis, p.d_vis, p.n_vis, p.ld_vis, p.a_vis, p.s_vis,
-                     p.sf_vis, p.zp_vis);
+  // ---- outlier paths and the low-rank operand row clear
+  if (wg == 0 && p.n_text > 0)
+    outlier_row_sm(p, row, xs, p.c_text, p.d_text, p.n_text, p.ld_text, p.a_text, p.s_text,
+                   p.sf_text, p.zp_text);
+  if (wg == (G > 1 ? 1 : 0) && p.n_vis > 0)
+    outlier_row_sm(p, row, xs, p.c_vis, p.d_vis, p.n_vis, p.ld_vis, p.a_vis, p.s_vis, p.sf_vis,
+                   p.zp_vis);
   if (p.k_lr > 0) {
     uint4* lr = reinterpret_cast<uint4*>(p.lr_a + (int64_t)row * p.k_lr);
-    for (int i = lane; i < p.k_lr / 8; i += 32) lr[i] = make_uint4(0, 0, 0, 0);
+    for (int i = tg; i < p.k_lr / 8; i += NTG) lr[i] = make_uint4(0, 0, 0, 0);
   }
   if (!mac) return;
 
-  // ---- pass 3 (text rows): residual codes at the aux width (layer.py:159-160);
-  // q is read back from this warp's own code row (same lanes, program order)
-  warp_minmax(elo, ehi);
-  double Se, zped;
-  const bool oke = group_params(elo, ehi, p.aux, &Se, &zped);
-  if (!oke) Se = 1.0;
-  const double rSe = __ddiv_rn(1.0, Se);
-  const int zpe = (int)zped;
+  // ---- pass 3 (text rows): residual codes (layer.py:159-160); q is read back
+  // from the code row this thread itself wrote (same addresses, program order)
+  group_minmax<G>(elo, ehi, red, g, wg);
+  bool oke;
+  const RowParams re = make_row_params(elo, ehi, p.aux, &oke);
   const bool cena = p.aux.centered != 0;
-  if (lane == 0) {
+  if (tg == 0) {
     if (!oke) atomicOr(p.err, ERR_SCALE_ZERO);
-    p.s_mac[cix] = Se;
-    p.zp_mac[cix] = zpe;
+    p.s_mac[cix] = re.S;
+    p.zp_mac[cix] = re.zp;
     int e;
-    frexp(S, &e);
-    p.lrs_mac[cix] = (float)(Se / ldexp(1.0, e - 1));
+    frexp(rp.S, &e);
+    p.lrs_mac[cix] = (float)(re.S / ldexp(1.0, e - 1));
   }
   int8_t* erow = p.a_mac + (int64_t)cix * ld;
-  for (int k0 = 4 * lane; k0 < ld; k0 += 128) {
+  for (int k0 = 4 * tg; k0 < ld; k0 += 4 * NTG) {
     double z[4];
-    gather4<T, GATHER>(p, xrow, k0, k0 + 3 < n_main, z);
+    gather4_smem<T, GATHER>(p, xs, k0, k0 + 3 < n_main, z);
     const uint32_t codes = *reinterpret_cast<const uint32_t*>(arow + k0);
-    uint32_t packed = 0;
+    double e[4];
+    int qe[4];
+    bool tie = false;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int c = cen ? (int)(int8_t)(codes >> (8 * u)) : (int)((codes >> (8 * u)) & 0xFF);
-      const int q = cen ? c + zp : c;
-      const double e = __dsub_rn(z[u], xh[q - qmin]);
-      const int qe = quant_lean(e, Se, rSe, zpe, p.aux.qmin, p.aux.qmax);
+      const int q = cen ? c + rp.zp : c;
+      e[u] = __dsub_rn(z[u], xh[min(max(q, rp.qmin), rp.qmax) - rp.qmin]);
+      qe[u] = quant_row(e[u], re, tie);
+    }
+    if (tie) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) qe[u] = quant_exact(e[u], re.S, 0.0, re.zp, re.qmin, re.qmax);
+    }
+    uint32_t packed = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
       const bool in = k0 + u < n_main;
-      packed |= (uint32_t)((in ? (cena ? qe - zpe : qe) : 0) & 0xFF) << (8 * u);
+      packed |= (uint32_t)((in ? (cena ? qe[u] - re.zp : qe[u]) : 0) & 0xFF) << (8 * u);
     }
     *reinterpret_cast<uint32_t*>(erow + k0) = packed;
   }
+}
+
+inline size_t k1_group_smem(int d_in, int esz, int G) {
+  const int row_bytes = (d_in * esz + 127) / 128 * 128;
+  return (size_t)(K1G_WARPS / G) * (row_bytes + 256 * 8 + 2 * G * 8 + 64);
 }
 
 }  // namespace splitq

@@ -460,36 +460,63 @@ int tile_n(int64_t n) { return (int)std::min<int64_t>(GEMM_MAX_BN, round_up(n, 1
 
 namespace {
 
-template <typename T, bool G>
-int launch_k1_t(const K1Params& k, cudaStream_t stream) {
-  const unsigned grid = (unsigned)((k.T + K1W_WARPS - 1) / K1W_WARPS);
-  k1_warp_kernel<T, G><<<grid, K1W_WARPS * 32, 0, stream>>>(k);
+template <typename T, bool GA, int G>
+int launch_k1_g(const K1Params& k, int d_in, cudaStream_t stream) {
+  const size_t smem = k1_group_smem(d_in, (int)sizeof(T), G);
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(k1_group_kernel<T, GA, G>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    attr = true;
+  }
+  constexpr int NG = K1G_WARPS / G;
+  const unsigned grid = (unsigned)((k.T + NG - 1) / NG);
+  k1_group_kernel<T, GA, G><<<grid, K1G_WARPS * 32, smem, stream>>>(k, d_in);
   CUDA_TRY(cudaGetLastError());
   return SPLITQ_OK;
 }
 
-template <bool G>
-int launch_k1_dt(const K1Params& k, cudaStream_t s) {
-  switch (k.x_dtype) {
-    case IN_F16: return launch_k1_t<__half, G>(k, s);
-    case IN_BF16: return launch_k1_t<__nv_bfloat16, G>(k, s);
-    case IN_F32: return launch_k1_t<float, G>(k, s);
-    default: return launch_k1_t<double, G>(k, s);
+template <typename T, bool GA>
+int launch_k1_t(const K1Params& k, int d_in, cudaStream_t s) {
+  // rows per group of G warps: keep one row's SMEM at most ~1/8 of the CTA budget
+  const int row_bytes = d_in * (int)sizeof(T);
+  const int G = row_bytes <= 12 * 1024 ? 1 : row_bytes <= 24 * 1024 ? 2
+              : row_bytes <= 48 * 1024 ? 4 : 8;
+  if (k1_group_smem(d_in, (int)sizeof(T), G) > 200 * 1024) return SPLITQ_ERR_UNSUPPORTED;
+  switch (G) {
+    case 1: return launch_k1_g<T, GA, 1>(k, d_in, s);
+    case 2: return launch_k1_g<T, GA, 2>(k, d_in, s);
+    case 4: return launch_k1_g<T, GA, 4>(k, d_in, s);
+    default: return launch_k1_g<T, GA, 8>(k, d_in, s);
   }
 }
 
-// K1 dispatch: warp-per-row kernel (generic per-row CTA kernel kept for code
-// matrices whose row stride is not a multiple of 16 bytes).
+template <bool GA>
+int launch_k1_dt(const K1Params& k, int d_in, cudaStream_t s) {
+  switch (k.x_dtype) {
+    case IN_F16: return launch_k1_t<__half, GA>(k, d_in, s);
+    case IN_BF16: return launch_k1_t<__nv_bfloat16, GA>(k, d_in, s);
+    case IN_F32: return launch_k1_t<float, GA>(k, d_in, s);
+    default: return launch_k1_t<double, GA>(k, d_in, s);
+  }
+}
+
+// K1 dispatch: the SMEM-staged row-group kernel; the generic per-row CTA
+// kernel (same arithmetic) covers code strides that are not 16-B multiples
+// and rows too large to stage.
 int launch_k1(const K1Params& k, int d_in, int device, cudaStream_t stream) {
-  (void)d_in;
   (void)device;
-  if (k.ld_main & 15) {
+  int rc = SPLITQ_ERR_UNSUPPORTED;
+  if ((k.ld_main & 15) == 0) {
+    rc = (k.c_main && k.d_main) ? launch_k1_dt<true>(k, d_in, stream)
+                                : launch_k1_dt<false>(k, d_in, stream);
+  }
+  if (rc == SPLITQ_ERR_UNSUPPORTED) {
     k1_quantize_kernel<<<(unsigned)k.T, K1_THREADS, 0, stream>>>(k);
     CUDA_TRY(cudaGetLastError());
     return SPLITQ_OK;
   }
-  if (k.c_main && k.d_main) return launch_k1_dt<true>(k, stream);
-  return launch_k1_dt<false>(k, stream);
+  return rc;
 }
 
 }  // namespace
