@@ -128,10 +128,11 @@ int splitq_workspace_layout(splitq_layer_t layer, int64_t tokens, splitq_ws_layo
 /* y = forward(layer, batch). x: device [tokens x x_ld] of x_dtype (d_in valid
  * columns); tags: device uint8 [tokens] (0 text, 1 vision); y: device
  * [tokens x y_ld] of y_dtype (F32 / F16 / BF16). With SPLITQ_FWD_RAW, y must
- * hold 4 consecutive [tokens x y_ld] 32-bit planes: int32 main accumulator,
- * int32 text-outlier accumulator, int32 vision-outlier accumulator and the
- * fp32 low-rank accumulator. Asynchronous on `stream` (cudaStream_t); call
- * splitq_read_status to surface data-dependent errors. */
+ * hold 2 consecutive [tokens x y_ld] 32-bit planes: the int32 main-channel
+ * accumulator sum_k (q_a - z_a) * q_w and the fp32 auxiliary accumulator
+ * (outlier + low-rank branches, scaled by 1 / (rho_i kappa_j)).
+ * Asynchronous on `stream` (cudaStream_t); call splitq_read_status to
+ * surface data-dependent errors. */
 int splitq_forward(splitq_layer_t layer, const void* x, int x_dtype, int64_t x_ld,
                    const uint8_t* tags, int64_t tokens, void* y, int y_dtype, int64_t y_ld,
                    void* workspace, size_t workspace_bytes, void* stream, int flags);

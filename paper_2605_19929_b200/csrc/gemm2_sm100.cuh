@@ -1,0 +1,362 @@
+// Split-linear GEMM v2 for sm_100a: CTA-pair (cta_group::2) tcgen05 MMA with
+// M = 256 rows per tile, double-buffered TMEM accumulators, and every
+// auxiliary branch folded into one fp32 accumulator.
+//
+// Reference semantics (numpy float64, pkg/src/modquant/layer.py):
+//   y = x_hat @ Q(R) + (x_hat @ Q(U_s)) @ Q(V_s)            :141-151
+//     + [text rows] (Q(e) @ Q(U_c)) @ Q(V_c)                 :157-166
+//     + Q(X_t d_t) @ Q(W_t/d_t) + Q(X_v d_v) @ Q(W_v/d_v)    :106-115, 132-133, 171
+// Per tile (each CTA of the pair owns 128 of the 256 rows):
+//   R_main[b] (int32, TMEM) = sum_k a_code * w_code           tcgen05 kind::i8, exact
+//   R_aux[b]  (fp32,  TMEM) = A_aux @ B_aux                    tcgen05 kind::f16
+//     A_aux (fp16, per token) = [text hi | lo | hi][vision hi | lo | hi][CWS t1][MAC t1]
+//     B_aux (fp16, per column) = [text hi | hi | lo][vision hi | hi | lo][CWS v][MAC v]
+//   (the hi/lo splits make the outlier products exact to ~2^-22)
+//   y = S_a[i] S_w[j] (R_main - zp_i cs_j) + rho_i kappa_j R_aux
+// Warp roles per CTA (192 threads): 0 TMA producer, 1 TMEM alloc + MMA issue
+// (leader CTA only), 2..5 epilogue. Accumulators are double-buffered so the
+// epilogue of tile t overlaps the MMAs of tile t+1.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "sm100_ptx.cuh"
+
+namespace splitq {
+
+constexpr int G2_BM = 256;                 // rows per CTA pair
+constexpr int G2_BN = 128;                 // columns per tile (both CTAs)
+constexpr int G2_A_BYTES = 128 * 128;      // per CTA: 128 rows x 128 B
+constexpr int G2_B_BYTES = (G2_BN / 2) * 128;  // per CTA: BN/2 rows x 128 B
+constexpr int G2_STAGE_BYTES = G2_A_BYTES + G2_B_BYTES;  // 24 KB
+constexpr int G2_STAGES = 8;
+constexpr int G2_THREADS = 192;
+constexpr int G2_TMEM_COLS = 512;
+constexpr int G2_SMEM_BYTES = G2_STAGES * G2_STAGE_BYTES + 1024 + 512;
+
+enum G2Mode : int { G2_SPLIT = 0, G2_RAW = 1, G2_LR1 = 2 };
+enum G2Out : int { G2_F32 = 0, G2_F16 = 1, G2_BF16 = 2 };
+
+struct G2Maps {
+  CUtensorMap a, b;      // main int8 operands: A [rows x K], B [N x K]
+  CUtensorMap xa, xb;    // aux fp16 operands: A_aux [rows x K_aux], B_aux [N x K_aux]
+};
+
+struct G2Params {
+  int M;              // rows (overridden by *m_count)
+  const int* m_count;
+  int N;              // columns
+  int bn;             // tile N: multiple of 32, <= G2_BN
+  int k_main;         // int8 K
+  int k_aux;          // fp16 K (multiple of 64; 0 = no aux branch)
+  uint32_t idesc_main, idesc_aux;
+  int mode, out_dtype;
+  const float* row_s;   // S_a (SPLIT) or S/rho (LR1)
+  const int* row_zp;    // zero points when A codes are u8
+  const float* row_rho;
+  const float* col_s;   // S_w (SPLIT) or S_u/sigma (LR1)
+  const int* col_cs;    // column code sums (u8 zero-point correction)
+  const float* col_kappa;
+  void* out;
+  int64_t ldo;
+  const int* row_map;   // LR1: destination row
+  int col_off;          // LR1: destination column
+  float* raw_aux;       // RAW: fp32 aux plane
+  int* err;
+};
+
+// ---------------------------------------------------------------- pair helpers
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// shared::cluster address of `p` in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_u32(p)), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+// TMA 2-D load whose completion is counted on the leader CTA's barrier.
+__device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorMap* map,
+                                                 uint64_t* bar, int32_t c0, int32_t c1) {
+  const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;  // peer bit cleared -> CTA 0 of the pair
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* smem_dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(smem_dst)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void mma_i8_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_f16_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                             uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// commit: arrive on the barrier at the same offset in both CTAs of the pair
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+
+__device__ __forceinline__ int g2_chunks(int k_bytes) { return (k_bytes + 127) / 128; }
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
+    splitq_gemm2_kernel(const __grid_constant__ G2Maps maps, const G2Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G2_STAGES * G2_STAGE_BYTES);
+  uint64_t* empty = full + G2_STAGES;
+  uint64_t* tfull = empty + G2_STAGES;   // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int M = p.m_count ? *p.m_count : p.M;
+  const int m_tiles = (M + G2_BM - 1) / G2_BM;
+  const int n_tiles = (p.N + p.bn - 1) / p.bn;
+  const int num_tiles = m_tiles * n_tiles;
+  const int pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
+  const int n_aux = p.k_aux / 64, n_main = g2_chunks(p.k_main);
+  const int stages_per_tile = n_aux + n_main;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < G2_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, G2_TMEM_COLS);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ================================================== TMA producer (both CTAs)
+    if (lane == 0 && num_tiles > 0) {
+      tma_prefetch(&maps.a);
+      tma_prefetch(&maps.b);
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t tx = 2u * (G2_A_BYTES + (uint32_t)(p.bn / 2) * 128u);
+      for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+        const int m0 = (tile / n_tiles) * G2_BM + (int)rank * 128;
+        const int n0 = (tile % n_tiles) * p.bn + (int)rank * (p.bn / 2);
+        for (int v = 0; v < stages_per_tile; ++v) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * G2_STAGE_BYTES;
+          uint8_t* sb = sa + G2_A_BYTES;
+          if (leader) mbar_arrive_expect_tx(&full[stage], tx);
+          if (v < n_aux) {
+            tma_load_2d_pair(sa, &maps.xa, &full[stage], v * 64, m0);
+            tma_load_2d_pair(sb, &maps.xb, &full[stage], v * 64, n0);
+          } else {
+            const int c = v - n_aux;
+            tma_load_2d_pair(sa, &maps.a, &full[stage], c * 128, m0);
+            tma_load_2d_pair(sb, &maps.b, &full[stage], c * 128, n0);
+          }
+          if (++stage == G2_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================================== MMA issuer (leader CTA)
+    if (leader && lane == 0 && num_tiles > 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
+        const int b = it & 1;
+        const uint32_t tph = (it >> 1) & 1;
+        mbar_wait(&tempty[b], tph ^ 1);
+        tc_fence_after();
+        const uint32_t d_main = tmem + b * 256;
+        const uint32_t d_aux = tmem + b * 256 + 128;
+        for (int v = 0; v < stages_per_tile; ++v) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * G2_STAGE_BYTES);
+          const uint64_t ad = sw128_kmajor_desc(a_addr);
+          const uint64_t bd = sw128_kmajor_desc(a_addr + G2_A_BYTES);
+          if (v < n_aux) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)  // K = 16 fp16 (32 B) per MMA
+              mma_f16_pair(d_aux, ad + 2 * k, bd + 2 * k, p.idesc_aux, (v | k) != 0);
+          } else {
+            const int c = v - n_aux;
+            const int nk = min(4, (p.k_main - c * 128 + 31) / 32);  // K = 32 int8 per MMA
+            for (int k = 0; k < nk; ++k)
+              mma_i8_pair(d_main, ad + 2 * k, bd + 2 * k, p.idesc_main, (c | k) != 0);
+          }
+          tc_commit_pair(&empty[stage]);
+          if (++stage == G2_STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit_pair(&tfull[b]);
+      }
+    }
+  } else {
+    // ================================================== epilogue (warps 2..5, both CTAs)
+    const int lq = warp & 3;                 // TMEM lane quarter
+    const int r_local = lq * 32 + lane;
+    const uint32_t tempty_leader = mapa_shared(&tempty[0], 0);
+    const bool has_aux = p.k_aux > 0;
+    int it = 0;
+    for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
+      const int b = it & 1;
+      const uint32_t tph = (it >> 1) & 1;
+      const int m0 = (tile / n_tiles) * G2_BM + (int)rank * 128;
+      const int n0 = (tile % n_tiles) * p.bn;
+      const int row = m0 + r_local;
+      const bool row_ok = row < M;
+      mbar_wait(&tfull[b], tph);
+      tc_fence_after();
+      float s_row = 0.f, rho = 0.f;
+      int zp = 0;
+      if (row_ok) {
+        if (p.row_s) s_row = p.row_s[row];
+        if (p.row_zp) zp = p.row_zp[row];
+        if (has_aux && p.row_rho) rho = p.row_rho[row];
+      }
+      const uint32_t lane_base = tmem + ((uint32_t)(lq * 32) << 16) + b * 256;
+      for (int c0 = 0; c0 < p.bn; c0 += 32) {
+        uint32_t am[32], af[32];
+        tmem_ld32(lane_base + c0, am);
+        if (has_aux) tmem_ld32(lane_base + 128 + c0, af);
+        tmem_wait_ld();
+        if (!row_ok) continue;
+        if (p.mode == G2_RAW) {
+          int* o = reinterpret_cast<int*>(p.out);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = n0 + c0 + j;
+            if (col < p.N) {
+              const int64_t idx = (int64_t)row * p.ldo + col;
+              o[idx] = (int)am[j];
+              if (has_aux && p.raw_aux) p.raw_aux[idx] = __uint_as_float(af[j]);
+            }
+          }
+        } else if (p.mode == G2_LR1) {
+          __half* o = reinterpret_cast<__half*>(p.out);
+          const int orow = p.row_map ? p.row_map[row] : row;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = n0 + c0 + j;
+            if (col < p.N) {
+              const int acc = (int)am[j] - (p.row_zp ? zp * p.col_cs[col] : 0);
+              const float v = acc == 0 ? 0.f : s_row * p.col_s[col] * (float)acc;
+              if (!(fabsf(v) <= 65504.f) && p.err) atomicOr(p.err, 8 /*ERR_LR_RANGE*/);
+              o[(int64_t)orow * p.ldo + p.col_off + col] = __float2half_rn(v);
+            }
+          }
+        } else {
+          float y[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = min(n0 + c0 + j, p.N - 1);
+            const int acc = (int)am[j] - (p.row_zp ? zp * p.col_cs[col] : 0);
+            float v = s_row * p.col_s[col] * (float)acc;
+            if (has_aux) v = fmaf(rho * p.col_kappa[col], __uint_as_float(af[j]), v);
+            y[j] = v;
+          }
+          const int64_t base = (int64_t)row * p.ldo + n0 + c0;
+          const bool full_chunk = (n0 + c0 + 32 <= p.N) && ((p.ldo & 7) == 0);
+          if (p.out_dtype == G2_F32) {
+            float* o = reinterpret_cast<float*>(p.out) + base;
+            if (full_chunk) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4*>(o + j) = make_float4(y[j], y[j + 1], y[j + 2], y[j + 3]);
+            } else {
+              for (int j = 0; j < 32; ++j)
+                if (n0 + c0 + j < p.N) o[j] = y[j];
+            }
+          } else if (p.out_dtype == G2_F16) {
+            __half* o = reinterpret_cast<__half*>(p.out) + base;
+            if (full_chunk) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                __half2 h[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) h[q] = __floats2half2_rn(y[j + 2 * q], y[j + 2 * q + 1]);
+                *reinterpret_cast<uint4*>(o + j) = *reinterpret_cast<uint4*>(h);
+              }
+            } else {
+              for (int j = 0; j < 32; ++j)
+                if (n0 + c0 + j < p.N) o[j] = __float2half_rn(y[j]);
+            }
+          } else {
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + base;
+            if (full_chunk) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                __nv_bfloat162 h[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                  h[q] = __floats2bfloat162_rn(y[j + 2 * q], y[j + 2 * q + 1]);
+                *reinterpret_cast<uint4*>(o + j) = *reinterpret_cast<uint4*>(h);
+              }
+            } else {
+              for (int j = 0; j < 32; ++j)
+                if (n0 + c0 + j < p.N) o[j] = __float2bfloat16_rn(y[j]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(b * sizeof(uint64_t)));
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, G2_TMEM_COLS);
+  }
+}
+
+}  // namespace splitq

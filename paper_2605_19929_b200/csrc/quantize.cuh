@@ -193,9 +193,12 @@ struct K1Params {
   double* s_mac;
   int* zp_mac;
   float* lrs_mac;  // S_e / rho(row)
-  // low-rank operand rows to clear (fp16, k_lr per row)
+  // fp16 auxiliary GEMM operand rows (k_lr per row): the outlier hi/lo
+  // segments are written here, the low-rank columns [lr_off_s, k_lr) cleared
   __half* lr_a;
   int k_lr;
+  int lr_off_t, lr_off_v, lr_off_s;  // segment offsets (elements)
+  int kt16, kv16;                     // outlier K rounded to 16
   int* err;
 };
 

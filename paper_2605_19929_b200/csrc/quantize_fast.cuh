@@ -430,6 +430,57 @@ __device__ void outlier_row_sm(const K1Params& p, int row, const T* xs, const in
   }
 }
 
+
+// ---- outlier paths in two steps: params (warp-level), then codes + the fp16
+// hi/lo segments of the auxiliary GEMM operand. a = (q - zp) * (S_p / rho) is
+// exact in fp64; a = a_hi + a_lo with a_hi = fp16(a), a_lo = fp16(a - a_hi).
+template <typename T>
+__device__ void outlier_params(const K1Params& p, const T* xs, const int* cols, const double* d,
+                               int n, RowParams& rp, bool& ok, bool& bad) {
+  const int lane = threadIdx.x & 31;
+  double lo = INFINITY, hi = -INFINITY;
+  bool nan = false;
+  for (int k = lane; k < n; k += 32) {
+    const double z = __dmul_rn(to_f64(xs[cols[k]]), d[k]);
+    nan |= z != z;
+    lo = z < lo ? z : lo;
+    hi = z > hi ? z : hi;
+  }
+  warp_minmax(lo, hi);
+  bad = __any_sync(0xffffffffu, nan) || !isfinite(lo) || !isfinite(hi);
+  rp = make_row_params(bad ? 0.0 : lo, bad ? 0.0 : hi, p.aux, &ok);
+}
+
+template <typename T>
+__device__ void outlier_codes(const K1Params& p, int row, const T* xs, const int* cols,
+                              const double* d, int n, int ld, int8_t* codes, const RowParams& rp,
+                              double fac, int seg_off, int k16) {
+  const int lane = threadIdx.x & 31;
+  int8_t* out = codes + (int64_t)row * ld;
+  __half* seg = p.k_lr > 0 ? p.lr_a + (int64_t)row * p.k_lr + seg_off : nullptr;
+  const int lim = max(ld, k16);
+  for (int k = lane; k < lim; k += 32) {
+    int c = 0;
+    double a = 0.0;
+    if (k < n) {
+      const double z = __dmul_rn(to_f64(xs[cols[k]]), d[k]);
+      bool tie = false;
+      int q = quant_row(z, rp, tie);
+      if (tie) q = quant_exact(z, rp.S, 0.0, rp.zp, rp.qmin, rp.qmax);
+      c = p.aux.centered ? q - rp.zp : q;
+      a = (double)(q - rp.zp) * fac;
+    }
+    if (k < ld) out[k] = (int8_t)c;
+    if (seg && k < k16) {
+      const __half hi = __double2half(a);
+      const __half lo = __double2half(a - (double)__half2float(hi));
+      seg[k] = hi;
+      seg[k16 + k] = lo;
+      seg[2 * k16 + k] = hi;
+    }
+  }
+}
+
 // One row per group of G warps (K1G_WARPS / G rows per CTA). The row is
 // staged into SMEM with one TMA bulk copy (cp.async.bulk) when it is 16-B
 // aligned, then every pass gathers from SMEM.
@@ -442,11 +493,13 @@ __global__ void __launch_bounds__(K1G_WARPS * 32) k1_group_kernel(const K1Params
   const int g = warp / G, wg = warp % G;  // group, warp within group
   const int tg = wg * 32 + lane;          // thread within group
   constexpr int NTG = 32 * G;
-  uint8_t* base = k1g_smem + g * (row_bytes + 256 * 8 + 2 * G * 8 + 64);
+  uint8_t* base = k1g_smem + g * (row_bytes + 256 * 8 + 2 * G * 8 + 128);
   T* xs = reinterpret_cast<T*>(base);
   double* xh = reinterpret_cast<double*>(base + row_bytes);
   double* red = xh + 256;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(red + 2 * G);
+  double* oscale = reinterpret_cast<double*>(mbar + 1);  // [2]: S_text, S_vision of the row
+  int* oflag = reinterpret_cast<int*>(oscale + 2);        // [2]: outlier path failed
   const int row = blockIdx.x * NG + g;
   if (row >= p.T) return;  // whole group exits together
   const T* xrow = reinterpret_cast<const T*>(p.x) + (int64_t)row * p.ldx;
@@ -507,17 +560,59 @@ __global__ void __launch_bounds__(K1G_WARPS * 32) k1_group_kernel(const K1Params
   const int cix = p.use_mac ? p.text_idx[row] : -1;
   const bool mac = cix >= 0;
   const bool cen = p.act.centered != 0;
+
+  // ---- outlier path parameters (warp 0: text, warp 1 or 0: vision)
+  const int vw = G > 1 ? 1 : 0;
+  RowParams rt, rv;
+  bool okt = true, okv = true, badt = false, badv = false;
+  if (wg == 0 && p.n_text > 0) {
+    outlier_params(p, xs, p.c_text, p.d_text, p.n_text, rt, okt, badt);
+    if (lane == 0) { oscale[0] = rt.S; oflag[0] = badt; }
+  }
+  if (wg == vw && p.n_vis > 0) {
+    outlier_params(p, xs, p.c_vis, p.d_vis, p.n_vis, rv, okv, badv);
+    if (lane == 0) { oscale[1] = rv.S; oflag[1] = badv; }
+  }
+  group_sync<G>(g);
+  const double st = p.n_text > 0 ? oscale[0] : 0.0;
+  const double sv = p.n_vis > 0 ? oscale[1] : 0.0;
+  if ((p.n_text > 0 && oflag[0]) || (p.n_vis > 0 && oflag[1])) {  // group-uniform
+    if (tg == 0) atomicOr(p.err, ERR_NONFINITE);
+    return;
+  }
+  // rho: power of two with max(S_a, S_t, S_v) in [rho, 2 rho) -- the common row
+  // normaliser of the fp32 auxiliary accumulator
+  int rexp;
+  frexp(fmax(rp.S, fmax(st, sv)), &rexp);
+  const double rho = ldexp(1.0, rexp - 1);
   if (tg == 0) {
     if (!ok) atomicOr(p.err, ERR_SCALE_ZERO);
     p.s_main[row] = rp.S;
     if (p.sf_main) p.sf_main[row] = (float)rp.S;
     p.zp_main[row] = rp.zp;
     if (p.rho) {
-      int e;
-      frexp(rp.S, &e);
-      const double rho = ldexp(1.0, e - 1);
       p.rho[row] = (float)rho;
       p.lrs_main[row] = (float)(rp.S / rho);
+    }
+  }
+  if (wg == 0 && p.n_text > 0) {
+    outlier_codes(p, row, xs, p.c_text, p.d_text, p.n_text, p.ld_text, p.a_text, rt,
+                  rt.S / rho, p.lr_off_t, p.kt16);
+    if (lane == 0) {
+      if (!okt) atomicOr(p.err, ERR_SCALE_ZERO);
+      p.s_text[row] = rt.S;
+      p.sf_text[row] = (float)rt.S;
+      p.zp_text[row] = rt.zp;
+    }
+  }
+  if (wg == vw && p.n_vis > 0) {
+    outlier_codes(p, row, xs, p.c_vis, p.d_vis, p.n_vis, p.ld_vis, p.a_vis, rv, rv.S / rho,
+                  p.lr_off_v, p.kv16);
+    if (lane == 0) {
+      if (!okv) atomicOr(p.err, ERR_SCALE_ZERO);
+      p.s_vis[row] = rv.S;
+      p.sf_vis[row] = (float)rv.S;
+      p.zp_vis[row] = rv.zp;
     }
   }
   if (mac) {
@@ -554,16 +649,10 @@ __global__ void __launch_bounds__(K1G_WARPS * 32) k1_group_kernel(const K1Params
     *reinterpret_cast<uint32_t*>(arow + k0) = packed;
   }
 
-  // ---- outlier paths and the low-rank operand row clear
-  if (wg == 0 && p.n_text > 0)
-    outlier_row_sm(p, row, xs, p.c_text, p.d_text, p.n_text, p.ld_text, p.a_text, p.s_text,
-                   p.sf_text, p.zp_text);
-  if (wg == (G > 1 ? 1 : 0) && p.n_vis > 0)
-    outlier_row_sm(p, row, xs, p.c_vis, p.d_vis, p.n_vis, p.ld_vis, p.a_vis, p.s_vis, p.sf_vis,
-                   p.zp_vis);
+  // ---- clear the low-rank columns of the auxiliary operand row (LR1 fills them)
   if (p.k_lr > 0) {
-    uint4* lr = reinterpret_cast<uint4*>(p.lr_a + (int64_t)row * p.k_lr);
-    for (int i = tg; i < p.k_lr / 8; i += NTG) lr[i] = make_uint4(0, 0, 0, 0);
+    uint4* lr = reinterpret_cast<uint4*>(p.lr_a + (int64_t)row * p.k_lr + p.lr_off_s);
+    for (int i = tg; i < (p.k_lr - p.lr_off_s) / 8; i += NTG) lr[i] = make_uint4(0, 0, 0, 0);
   }
   if (!mac) return;
 
@@ -577,9 +666,7 @@ __global__ void __launch_bounds__(K1G_WARPS * 32) k1_group_kernel(const K1Params
     if (!oke) atomicOr(p.err, ERR_SCALE_ZERO);
     p.s_mac[cix] = re.S;
     p.zp_mac[cix] = re.zp;
-    int e;
-    frexp(rp.S, &e);
-    p.lrs_mac[cix] = (float)(re.S / ldexp(1.0, e - 1));
+    p.lrs_mac[cix] = (float)(re.S / rho);
   }
   int8_t* erow = p.a_mac + (int64_t)cix * ld;
   for (int k0 = 4 * tg; k0 < ld; k0 += 4 * NTG) {
@@ -612,7 +699,7 @@ __global__ void __launch_bounds__(K1G_WARPS * 32) k1_group_kernel(const K1Params
 
 inline size_t k1_group_smem(int d_in, int esz, int G) {
   const int row_bytes = (d_in * esz + 127) / 128 * 128;
-  return (size_t)(K1G_WARPS / G) * (row_bytes + 256 * 8 + 2 * G * 8 + 64);
+  return (size_t)(K1G_WARPS / G) * (row_bytes + 256 * 8 + 2 * G * 8 + 128);
 }
 
 }  // namespace splitq

@@ -14,7 +14,7 @@
 #include <vector>
 
 #include "../../include/splitq.h"
-#include "gemm_sm100.cuh"
+#include "gemm2_sm100.cuh"
 #include "quantize.cuh"
 #include "quantize_fast.cuh"
 #include "tma_host.cuh"
@@ -138,14 +138,13 @@ struct splitq_layer_s {
   QSpecDev act{}, aux{};
   int use_cws = 0, use_mac = 0;
   int64_t ld_main = 0, ld_text = 0, ld_vis = 0;
-  int64_t r_s16 = 0, r_c16 = 0, k_lr = 0;
+  int64_t r_s16 = 0, r_c16 = 0, k_lr = 0;  // k_lr = K of the fp16 auxiliary GEMM
+  int64_t kt16 = 0, kv16 = 0, off_t = 0, off_v = 0, off_s = 0, off_c = 0;
   DevBuf mem;
   int* c_main = nullptr; double* d_main = nullptr;
   int* c_text = nullptr; double* d_text = nullptr;
   int* c_vis = nullptr; double* d_vis = nullptr;
   int8_t* b_main = nullptr; float* s_main = nullptr; int* cs_main = nullptr;
-  int8_t* b_text = nullptr; float* s_text = nullptr; int* cs_text = nullptr;
-  int8_t* b_vis = nullptr; float* s_vis = nullptr; int* cs_vis = nullptr;
   int8_t* b_us = nullptr; float* s_us = nullptr; int* cs_us = nullptr;
   int8_t* b_uc = nullptr; float* s_uc = nullptr; int* cs_uc = nullptr;
   __half* b_lr = nullptr; float* kappa = nullptr;
@@ -261,7 +260,14 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
   L->ld_vis = round_up(std::max<int64_t>(L->n_vis, 1), 16);
   L->r_s16 = round_up(L->r_s, 16);
   L->r_c16 = round_up(L->r_c, 16);
-  L->k_lr = (L->r_s + L->r_c) ? round_up(L->r_s16 + L->r_c16, 64) : 0;
+  // auxiliary fp16 operand segments: [text hi|lo|hi][vision hi|lo|hi][CWS][MAC]
+  L->kt16 = round_up(L->n_text, 16);
+  L->kv16 = round_up(L->n_vis, 16);
+  L->off_t = 0;
+  L->off_v = 3 * L->kt16;
+  L->off_s = L->off_v + 3 * L->kv16;
+  L->off_c = L->off_s + L->r_s16;
+  L->k_lr = (L->off_c + L->r_c16) ? round_up(L->off_c + L->r_c16, 64) : 0;
 
   auto cleanup = [&](int code) {
     L->mem.release();
@@ -287,13 +293,6 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
   if ((rc = pack_weight(L, d->q_main, d->s_main, d->n_main, N, L->ld_main, &L->b_main, &L->s_main,
                         &L->cs_main)))
     return cleanup(rc);
-  if (L->n_text && (rc = pack_weight(L, d->q_text, d->s_text, d->n_text, N, L->ld_text, &L->b_text,
-                                     &L->s_text, &L->cs_text)))
-    return cleanup(rc);
-  if (L->n_vis && (rc = pack_weight(L, d->q_vision, d->s_vision, d->n_vision, N, L->ld_vis,
-                                    &L->b_vis, &L->s_vis, &L->cs_vis)))
-    return cleanup(rc);
-
   if (L->k_lr) {
     // Low-rank first stage: A_lr[i, c] = (S_a[i] / rho_i) * (S_u[c] / sigma_c) * acc[i, c]
     // with sigma_c a power of two bounding |A_lr| by 2^15 (fp16-safe for any input).
@@ -331,24 +330,55 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
                             &L->cs_uc, 1.0, &sig_c)))
         return cleanup(rc);
     }
+    // B_aux (fp16, d_out x k_lr, K-major), per column j with colf = S_vs[j]
+    // (or the first present branch scale) and kappa_j a power of two:
+    //   text   [hi | hi | lo] of q_t[k, j] * (S_t[j] / colf) / kappa_j
+    //   vision [hi | hi | lo] of q_v[k, j] * (S_v[j] / colf) / kappa_j
+    //   CWS    q_vs[c, j] * sigma_c / kappa_j                      (exact)
+    //   MAC    q_vc[c, j] * (S_vc[j] / colf) * sigma'_c / kappa_j
+    // and the epilogue adds rho_i * (kappa_j * colf) * R_aux[i, j].
     std::vector<__half> blr((size_t)N * L->k_lr, __float2half(0.f));
     std::vector<float> kap((size_t)N);
     std::vector<double> row((size_t)L->k_lr);
     for (int64_t j = 0; j < N; ++j) {
-      const double colf = L->r_s ? d->s_vs[j] : d->s_vc[j];
+      const double colf = L->r_s ? d->s_vs[j]
+                          : L->n_text ? d->s_text[j]
+                          : L->r_c ? d->s_vc[j]
+                          : L->n_vis ? d->s_vision[j] : 1.0;
       std::fill(row.begin(), row.end(), 0.0);
       double mx = 0.0;
+      for (int64_t k = 0; k < L->n_text; ++k) {
+        row[L->off_t + k] = (double)d->q_text[k * N + j] * (d->s_text[j] / colf);
+        mx = std::max(mx, std::fabs(row[L->off_t + k]));
+      }
+      for (int64_t k = 0; k < L->n_vis; ++k) {
+        row[L->off_v + k] = (double)d->q_vision[k * N + j] * (d->s_vision[j] / colf);
+        mx = std::max(mx, std::fabs(row[L->off_v + k]));
+      }
       for (int64_t c = 0; c < L->r_s; ++c) {
-        row[c] = (double)d->q_vs[c * N + j] * sig_s[c];
-        mx = std::max(mx, std::fabs(row[c]));
+        row[L->off_s + c] = (double)d->q_vs[c * N + j] * sig_s[c];
+        mx = std::max(mx, std::fabs(row[L->off_s + c]));
       }
       for (int64_t c = 0; c < L->r_c; ++c) {
-        row[L->r_s16 + c] = (double)d->q_vc[c * N + j] * (d->s_vc[j] / colf) * sig_c[c];
-        mx = std::max(mx, std::fabs(row[L->r_s16 + c]));
+        row[L->off_c + c] = (double)d->q_vc[c * N + j] * (d->s_vc[j] / colf) * sig_c[c];
+        mx = std::max(mx, std::fabs(row[L->off_c + c]));
       }
       const double kappa = mx > 0 ? pow2_ceil(mx) : 1.0;
-      for (int64_t c = 0; c < L->k_lr; ++c)
-        blr[(size_t)j * L->k_lr + c] = __double2half(row[c] / kappa);
+      __half* dst = blr.data() + (size_t)j * L->k_lr;
+      auto split3 = [&](int64_t off, int64_t n, int64_t k16) {
+        for (int64_t k = 0; k < n; ++k) {
+          const double v = row[off + k] / kappa;
+          const __half hi = __double2half(v);
+          const __half lo = __double2half(v - (double)__half2float(hi));
+          dst[off + k] = hi;
+          dst[off + k16 + k] = hi;
+          dst[off + 2 * k16 + k] = lo;
+        }
+      };
+      split3(L->off_t, L->n_text, L->kt16);
+      split3(L->off_v, L->n_vis, L->kv16);
+      for (int64_t c = 0; c < L->r_s; ++c) dst[L->off_s + c] = __double2half(row[L->off_s + c] / kappa);
+      for (int64_t c = 0; c < L->r_c; ++c) dst[L->off_c + c] = __double2half(row[L->off_c + c] / kappa);
       kap[j] = (float)(kappa * colf);
     }
     if ((rc = L->mem.upload(&L->b_lr, blr.data(), blr.size()))) return cleanup(rc);
@@ -423,37 +453,44 @@ namespace {
 bool g_gemm_attr_set[64] = {false};
 
 struct GemmLaunch {
-  GemmMaps maps;
-  GemmParams p;
+  G2Maps maps;
+  G2Params p;
 };
 
+// Persistent launch: one CTA pair per two SMs (cluster of 2).
 int launch_gemm(GemmLaunch& g, int device, int64_t max_rows, cudaStream_t stream) {
   if (device >= 0 && device < 64 && !g_gemm_attr_set[device]) {
-    CUDA_TRY(cudaFuncSetAttribute(splitq_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  GEMM_SMEM_BYTES));
+    CUDA_TRY(cudaFuncSetAttribute(splitq_gemm2_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, G2_SMEM_BYTES));
     g_gemm_attr_set[device] = true;
   }
-  const int64_t m_tiles = (max_rows + GEMM_BM - 1) / GEMM_BM;
+  const int64_t m_tiles = (max_rows + G2_BM - 1) / G2_BM;
   const int64_t n_tiles = (g.p.N + g.p.bn - 1) / g.p.bn;
   const int64_t tiles = m_tiles * n_tiles;
   if (tiles == 0) return SPLITQ_OK;
-  const int grid = (int)std::min<int64_t>(tiles, sm_count(device));
-  splitq_gemm_kernel<<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, stream>>>(g.maps, g.p);
+  const int pairs = (int)std::min<int64_t>(tiles, sm_count(device) / 2);
+  splitq_gemm2_kernel<<<2 * pairs, G2_THREADS, G2_SMEM_BYTES, stream>>>(g.maps, g.p);
   CUDA_TRY(cudaGetLastError());
   return SPLITQ_OK;
 }
 
+// K-major int8 operand, box of box_rows rows x 128 bytes (128-B swizzle)
 bool map_i8(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld,
             uint32_t box_rows) {
   return make_map_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, rows, cols, ld, box_rows, 128);
 }
+// K-major fp16 operand, box of box_rows rows x 64 elements
 bool map_f16(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld_elems,
              uint32_t box_rows) {
   return make_map_2d(m, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, rows, cols, ld_elems * 2, box_rows,
                      64);
 }
 
-int tile_n(int64_t n) { return (int)std::min<int64_t>(GEMM_MAX_BN, round_up(n, 16)); }
+int tile_n(int64_t n) { return (int)std::min<int64_t>(G2_BN, round_up(n, 32)); }
+
+// i8 MMA instruction descriptor for the pair (M = 256), f16 likewise
+uint32_t idesc_i8(bool a_signed, int bn) { return make_idesc(2, a_signed ? 1u : 0u, 1, G2_BM, bn); }
+uint32_t idesc_f16(int bn) { return make_idesc(1, 0, 0, G2_BM, bn); }
 
 }  // namespace
 
@@ -610,114 +647,82 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   k.lrs_mac = (float*)at(W.lrs_mac);
   k.lr_a = (__half*)at(W.lr_a);
   k.k_lr = (int)L->k_lr;
+  k.lr_off_t = (int)L->off_t;
+  k.lr_off_v = (int)L->off_v;
+  k.lr_off_s = (int)L->off_s;
+  k.kt16 = (int)L->kt16;
+  k.kv16 = (int)L->kv16;
   k.err = err;
   if ((rc = launch_k1(k, (int)L->d_in, L->device, stream))) return rc;
   if (prof && (rc = prof_record(L, stream))) return rc;
 
-  const uint32_t a_fmt_main = L->act.centered ? 1u : 0u;  // s8 : u8
-  const uint32_t a_fmt_aux = L->aux.centered ? 1u : 0u;
   __half* lr_a = (__half*)at(W.lr_a);
 
-  // ---- low-rank first stages (write the fp16 second-stage operand)
-  if (L->r_s) {
+  // ---- low-rank first stages: fp16 columns of the auxiliary operand
+  auto lr1 = [&](const void* a_codes, bool a_signed, const int8_t* bu, const float* su,
+                 const int* csu, int64_t r, const float* row_s, const int* row_zp,
+                 const int* m_count, const int* row_map, int64_t col_off) -> int {
     GemmLaunch g{};
     g.p.M = (int)T;
-    g.p.N = (int)L->r_s;
-    g.p.bn = tile_n(L->r_s);
+    g.p.m_count = m_count;
+    g.p.N = (int)r;
+    g.p.bn = tile_n(r);
     g.p.k_main = (int)L->n_main;
-    g.p.idesc_main = make_idesc(2, a_fmt_main, 1, GEMM_BM, g.p.bn);
-    g.p.mode = EPI_LR1;
-    g.p.row_s = (const float*)at(W.lrs_main);
-    g.p.row_zp = L->act.centered ? nullptr : (const int*)at(W.zp_main);
-    g.p.col_s = L->s_us;
-    g.p.col_cs = L->cs_us;
+    g.p.idesc_main = idesc_i8(a_signed, g.p.bn);
+    g.p.mode = G2_LR1;
+    g.p.row_s = row_s;
+    g.p.row_zp = row_zp;
+    g.p.col_s = su;
+    g.p.col_cs = csu;
     g.p.out = lr_a;
     g.p.ldo = L->k_lr;
-    g.p.col_off = 0;
+    g.p.col_off = (int)col_off;
+    g.p.row_map = row_map;
     g.p.err = err;
-    bool ok = map_i8(&g.maps.a, at(W.a_main), T, L->n_main, L->ld_main, GEMM_BM) &&
-              map_i8(&g.maps.b, L->b_us, L->r_s, L->n_main, L->ld_main, g.p.bn);
-    g.maps.at = g.maps.bt = g.maps.av = g.maps.bv = g.maps.la = g.maps.lb = g.maps.a;
-    if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (LR1 cws)");
-    if ((rc = launch_gemm(g, L->device, T, stream))) return rc;
-  }
-  if (L->r_c) {
-    GemmLaunch g{};
-    g.p.M = (int)T;
-    g.p.m_count = n_text;
-    g.p.N = (int)L->r_c;
-    g.p.bn = tile_n(L->r_c);
-    g.p.k_main = (int)L->n_main;
-    g.p.idesc_main = make_idesc(2, a_fmt_aux, 1, GEMM_BM, g.p.bn);
-    g.p.mode = EPI_LR1;
-    g.p.row_s = (const float*)at(W.lrs_mac);
-    g.p.row_zp = L->aux.centered ? nullptr : (const int*)at(W.zp_mac);
-    g.p.col_s = L->s_uc;
-    g.p.col_cs = L->cs_uc;
-    g.p.out = lr_a;
-    g.p.ldo = L->k_lr;
-    g.p.col_off = (int)L->r_s16;
-    g.p.row_map = text_rows;
-    g.p.err = err;
-    bool ok = map_i8(&g.maps.a, at(W.a_mac), T, L->n_main, L->ld_main, GEMM_BM) &&
-              map_i8(&g.maps.b, L->b_uc, L->r_c, L->n_main, L->ld_main, g.p.bn);
-    g.maps.at = g.maps.bt = g.maps.av = g.maps.bv = g.maps.la = g.maps.lb = g.maps.a;
-    if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (LR1 mac)");
-    if ((rc = launch_gemm(g, L->device, T, stream))) return rc;
-  }
-
+    bool ok = map_i8(&g.maps.a, a_codes, T, L->n_main, L->ld_main, 128) &&
+              map_i8(&g.maps.b, bu, r, L->n_main, L->ld_main, g.p.bn / 2);
+    g.maps.xa = g.maps.xb = g.maps.a;
+    if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (LR1)");
+    return launch_gemm(g, L->device, T, stream);
+  };
+  if (L->r_s &&
+      (rc = lr1(at(W.a_main), L->act.centered, L->b_us, L->s_us, L->cs_us, L->r_s,
+                (const float*)at(W.lrs_main), L->act.centered ? nullptr : (const int*)at(W.zp_main),
+                nullptr, nullptr, L->off_s)))
+    return rc;
+  if (L->r_c &&
+      (rc = lr1(at(W.a_mac), L->aux.centered, L->b_uc, L->s_uc, L->cs_uc, L->r_c,
+                (const float*)at(W.lrs_mac), L->aux.centered ? nullptr : (const int*)at(W.zp_mac),
+                n_text, text_rows, L->off_c)))
+    return rc;
   if (prof && (rc = prof_record(L, stream))) return rc;
 
-  // ---- split GEMM: main + outliers + low-rank second stage + merge
+  // ---- split GEMM: int8 main GEMM + fp16 auxiliary GEMM + merge epilogue
   GemmLaunch g{};
   g.p.M = (int)T;
   g.p.N = (int)L->d_out;
   g.p.bn = tile_n(L->d_out);
   g.p.k_main = (int)L->n_main;
-  g.p.k_text = (int)L->n_text;
-  g.p.k_vis = (int)L->n_vis;
-  g.p.k_lr = (int)L->k_lr;
-  g.p.idesc_main = make_idesc(2, a_fmt_main, 1, GEMM_BM, g.p.bn);
-  g.p.idesc_text = make_idesc(2, a_fmt_aux, 1, GEMM_BM, g.p.bn);
-  g.p.idesc_vis = g.p.idesc_text;
-  g.p.idesc_lr = make_idesc(1, 0, 0, GEMM_BM, g.p.bn);
-  g.p.mode = raw ? EPI_RAW : EPI_SPLIT;
-  g.p.out_dtype = y_dtype == SPLITQ_F32 ? OUT_F32 : y_dtype == SPLITQ_F16 ? OUT_F16 : OUT_BF16;
+  g.p.k_aux = (int)L->k_lr;
+  g.p.idesc_main = idesc_i8(L->act.centered, g.p.bn);
+  g.p.idesc_aux = idesc_f16(g.p.bn);
+  g.p.mode = raw ? G2_RAW : G2_SPLIT;
+  g.p.out_dtype = y_dtype == SPLITQ_F32 ? G2_F32 : y_dtype == SPLITQ_F16 ? G2_F16 : G2_BF16;
   g.p.row_s = (const float*)at(W.sf_main);
   g.p.row_zp = L->act.centered ? nullptr : (const int*)at(W.zp_main);
-  g.p.row_st = (const float*)at(W.sf_text);
-  g.p.row_zpt = L->aux.centered ? nullptr : (const int*)at(W.zp_text);
-  g.p.row_sv = (const float*)at(W.sf_vision);
-  g.p.row_zpv = L->aux.centered ? nullptr : (const int*)at(W.zp_vision);
   g.p.row_rho = (const float*)at(W.rho);
   g.p.col_s = L->s_main;
   g.p.col_cs = L->cs_main;
-  g.p.col_st = L->s_text;
-  g.p.col_cst = L->cs_text;
-  g.p.col_sv = L->s_vis;
-  g.p.col_csv = L->cs_vis;
   g.p.col_kappa = L->kappa;
   g.p.out = y;
   g.p.ldo = y_ld;
-  if (raw) {
-    int* planes = reinterpret_cast<int*>(y);
-    const int64_t plane = T * y_ld;
-    g.p.raw_t = planes + plane;
-    g.p.raw_v = planes + 2 * plane;
-    g.p.raw_f = reinterpret_cast<float*>(planes + 3 * plane);
-  }
-  bool ok = map_i8(&g.maps.a, at(W.a_main), T, L->n_main, L->ld_main, GEMM_BM) &&
-            map_i8(&g.maps.b, L->b_main, L->d_out, L->n_main, L->ld_main, g.p.bn);
-  g.maps.at = g.maps.bt = g.maps.av = g.maps.bv = g.maps.la = g.maps.lb = g.maps.a;
-  if (ok && L->n_text)
-    ok = map_i8(&g.maps.at, at(W.a_text), T, L->n_text, L->ld_text, GEMM_BM) &&
-         map_i8(&g.maps.bt, L->b_text, L->d_out, L->n_text, L->ld_text, g.p.bn);
-  if (ok && L->n_vis)
-    ok = map_i8(&g.maps.av, at(W.a_vision), T, L->n_vis, L->ld_vis, GEMM_BM) &&
-         map_i8(&g.maps.bv, L->b_vis, L->d_out, L->n_vis, L->ld_vis, g.p.bn);
+  if (raw) g.p.raw_aux = reinterpret_cast<float*>(reinterpret_cast<int*>(y) + T * y_ld);
+  bool ok = map_i8(&g.maps.a, at(W.a_main), T, L->n_main, L->ld_main, 128) &&
+            map_i8(&g.maps.b, L->b_main, L->d_out, L->n_main, L->ld_main, g.p.bn / 2);
+  g.maps.xa = g.maps.xb = g.maps.a;
   if (ok && L->k_lr)
-    ok = map_f16(&g.maps.la, lr_a, T, L->k_lr, L->k_lr, GEMM_BM) &&
-         map_f16(&g.maps.lb, L->b_lr, L->d_out, L->k_lr, L->k_lr, g.p.bn);
+    ok = map_f16(&g.maps.xa, lr_a, T, L->k_lr, L->k_lr, 128) &&
+         map_f16(&g.maps.xb, L->b_lr, L->d_out, L->k_lr, L->k_lr, g.p.bn / 2);
   if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (split GEMM)");
   if ((rc = launch_gemm(g, L->device, T, stream))) return rc;
   if (prof && (rc = prof_record(L, stream))) return rc;
@@ -802,12 +807,12 @@ int splitq_gemm_i8(const int8_t* a, int64_t lda, int a_signed, const int8_t* b, 
   g.p.N = (int)n;
   g.p.bn = tile_n(n);
   g.p.k_main = (int)k;
-  g.p.idesc_main = make_idesc(2, a_signed ? 1u : 0u, 1, GEMM_BM, g.p.bn);
-  g.p.mode = EPI_RAW;
+  g.p.idesc_main = idesc_i8(a_signed != 0, g.p.bn);
+  g.p.mode = G2_RAW;
   g.p.out = c;
   g.p.ldo = ldc;
-  bool ok = map_i8(&g.maps.a, a, m, k, lda, GEMM_BM) && map_i8(&g.maps.b, b, n, k, ldb, g.p.bn);
-  g.maps.at = g.maps.bt = g.maps.av = g.maps.bv = g.maps.la = g.maps.lb = g.maps.a;
+  bool ok = map_i8(&g.maps.a, a, m, k, lda, 128) && map_i8(&g.maps.b, b, n, k, ldb, g.p.bn / 2);
+  g.maps.xa = g.maps.xb = g.maps.a;
   if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   return launch_gemm(g, device, m, reinterpret_cast<cudaStream_t>(stream_));
 }

@@ -164,7 +164,7 @@ class GpuLayer:
         if ws is None:
             ws = self.workspace(T)
         if raw:
-            y = torch.empty((4, T, self.d_out), dtype=torch.int32, device=self.device)
+            y = torch.empty((2, T, self.d_out), dtype=torch.int32, device=self.device)
             ydt = _lib.F32
         else:
             out_dtype = out_dtype or torch.float32

@@ -111,12 +111,11 @@ def _check_acc(layer, x, tags):
             return acc[name]
         return acc[name] + act[name][2][:, None] * w[name][0].sum(axis=0)[None, :]
 
+    # the int32 main-channel accumulator is bit-exact (north-star bar); the
+    # outlier / low-rank branches share the fp32 auxiliary accumulator and are
+    # covered by the output tolerance test
     np.testing.assert_array_equal(planes[0], expect("main", lay.code_centered_main))
-    if "text" in acc:
-        np.testing.assert_array_equal(planes[1], expect("text", lay.code_centered_aux))
-    if "vision" in acc:
-        np.testing.assert_array_equal(planes[2], expect("vision", lay.code_centered_aux))
-    assert planes.shape == (4, T, L.d_out)
+    assert planes.shape == (2, T, L.d_out)
 
 
 def _check_out(layer, x, tags, out_dtype=None):
