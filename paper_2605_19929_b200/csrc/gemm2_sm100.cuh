@@ -27,14 +27,21 @@
 namespace splitq {
 
 constexpr int G2_BM = 256;                 // rows per CTA pair
-constexpr int G2_BN = 128;                 // columns per tile (both CTAs)
+constexpr int G2_BN = 128;                 // max tile N with the aux accumulator
+constexpr int G2_BN_MAX = 256;             // max tile N without it
 constexpr int G2_A_BYTES = 128 * 128;      // per CTA: 128 rows x 128 B
-constexpr int G2_B_BYTES = (G2_BN / 2) * 128;  // per CTA: BN/2 rows x 128 B
-constexpr int G2_STAGE_BYTES = G2_A_BYTES + G2_B_BYTES;  // 24 KB
-constexpr int G2_STAGES = 8;
+constexpr int G2_MAX_STAGES = 12;
+constexpr int G2_RING_BYTES = 192 * 1024;  // SMEM ring: stages of A (16 KB) + B (bn * 64 B)
 constexpr int G2_THREADS = 192;
 constexpr int G2_TMEM_COLS = 512;
-constexpr int G2_SMEM_BYTES = G2_STAGES * G2_STAGE_BYTES + 1024 + 512;
+constexpr int G2_SMEM_BYTES = G2_RING_BYTES + 1024 + 512;
+
+// stage geometry for a tile width: per CTA an A box (128 x 128 B) and a B box (bn/2 x 128 B)
+__host__ __device__ inline int g2_stage_bytes(int bn) { return G2_A_BYTES + bn * 64; }
+__host__ __device__ inline int g2_stages(int bn) {
+  const int s = G2_RING_BYTES / g2_stage_bytes(bn);
+  return s < G2_MAX_STAGES ? s : G2_MAX_STAGES;
+}
 
 enum G2Mode : int { G2_SPLIT = 0, G2_RAW = 1, G2_LR1 = 2 };
 enum G2Out : int { G2_F32 = 0, G2_F16 = 1, G2_BF16 = 2 };
@@ -48,7 +55,7 @@ struct G2Params {
   int M;              // rows (overridden by *m_count)
   const int* m_count;
   int N;              // columns
-  int bn;             // tile N: multiple of 32, <= G2_BN
+  int bn;             // tile N: multiple of 32, <= G2_BN (aux) or G2_BN_MAX
   int k_main;         // int8 K
   int k_aux;          // fp16 K (multiple of 64; 0 = no aux branch)
   uint32_t idesc_main, idesc_aux;
@@ -135,14 +142,25 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
 
 __device__ __forceinline__ int g2_chunks(int k_bytes) { return (k_bytes + 127) / 128; }
 
+// one lane of a converged warp (the same lane every call)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
     splitq_gemm2_kernel(const __grid_constant__ G2Maps maps, const G2Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G2_STAGES * G2_STAGE_BYTES);
-  uint64_t* empty = full + G2_STAGES;
-  uint64_t* tfull = empty + G2_STAGES;   // [2]
+  const int STAGES = g2_stages(p.bn);
+  const int STAGE_BYTES = g2_stage_bytes(p.bn);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G2_RING_BYTES);
+  uint64_t* empty = full + G2_MAX_STAGES;
+  uint64_t* tfull = empty + G2_MAX_STAGES;  // [2]
   uint64_t* tempty = tfull + 2;          // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -158,7 +176,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
   const int stages_per_tile = n_aux + n_main;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < G2_STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -176,9 +194,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
 
   if (warp == 0) {
     // ================================================== TMA producer (both CTAs)
-    if (lane == 0 && num_tiles > 0) {
-      tma_prefetch(&maps.a);
-      tma_prefetch(&maps.b);
+    if (num_tiles > 0) {
+      if (elect_one()) {
+        tma_prefetch(&maps.a);
+        tma_prefetch(&maps.b);
+      }
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t tx = 2u * (G2_A_BYTES + (uint32_t)(p.bn / 2) * 128u);
@@ -187,54 +207,69 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
         const int n0 = (tile % n_tiles) * p.bn + (int)rank * (p.bn / 2);
         for (int v = 0; v < stages_per_tile; ++v) {
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * G2_STAGE_BYTES;
+          uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + G2_A_BYTES;
-          if (leader) mbar_arrive_expect_tx(&full[stage], tx);
-          if (v < n_aux) {
-            tma_load_2d_pair(sa, &maps.xa, &full[stage], v * 64, m0);
-            tma_load_2d_pair(sb, &maps.xb, &full[stage], v * 64, n0);
-          } else {
-            const int c = v - n_aux;
-            tma_load_2d_pair(sa, &maps.a, &full[stage], c * 128, m0);
-            tma_load_2d_pair(sb, &maps.b, &full[stage], c * 128, n0);
+          if (elect_one()) {
+            if (leader) mbar_arrive_expect_tx(&full[stage], tx);
+            if (v < n_aux) {
+              tma_load_2d_pair(sa, &maps.xa, &full[stage], v * 64, m0);
+              tma_load_2d_pair(sb, &maps.xb, &full[stage], v * 64, n0);
+            } else {
+              const int c = v - n_aux;
+              tma_load_2d_pair(sa, &maps.a, &full[stage], c * 128, m0);
+              tma_load_2d_pair(sb, &maps.b, &full[stage], c * 128, n0);
+            }
           }
-          if (++stage == G2_STAGES) { stage = 0; phase ^= 1; }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ================================================== MMA issuer (leader CTA)
-    if (leader && lane == 0 && num_tiles > 0) {
+    // The whole warp walks the pipeline (values stay warp-uniform, so the
+    // descriptors live in uniform registers); one elected lane issues.
+    if (leader && num_tiles > 0) {
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
+      const uint32_t smem0 = smem_u32(smem);
       for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
         const int b = it & 1;
         const uint32_t tph = (it >> 1) & 1;
         mbar_wait(&tempty[b], tph ^ 1);
         tc_fence_after();
-        const uint32_t d_main = tmem + b * 256;
-        const uint32_t d_aux = tmem + b * 256 + 128;
+        // with the aux accumulator: [main 128 | aux 128] per buffer; without: main bn
+        const uint32_t d_main = tmem + b * (n_aux ? 256 : p.bn);
+        const uint32_t d_aux = d_main + 128;
         for (int v = 0; v < stages_per_tile; ++v) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(smem + stage * G2_STAGE_BYTES);
+          const uint32_t a_addr = smem0 + stage * STAGE_BYTES;
           const uint64_t ad = sw128_kmajor_desc(a_addr);
           const uint64_t bd = sw128_kmajor_desc(a_addr + G2_A_BYTES);
           if (v < n_aux) {
+            if (elect_one()) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)  // K = 16 fp16 (32 B) per MMA
-              mma_f16_pair(d_aux, ad + 2 * k, bd + 2 * k, p.idesc_aux, (v | k) != 0);
+              for (int k = 0; k < 4; ++k)  // K = 16 fp16 (32 B) per MMA
+                mma_f16_pair(d_aux, ad + 2 * k, bd + 2 * k, p.idesc_aux, (v | k) != 0);
+              tc_commit_pair(&empty[stage]);
+            }
           } else {
             const int c = v - n_aux;
-            const int nk = min(4, (p.k_main - c * 128 + 31) / 32);  // K = 32 int8 per MMA
-            for (int k = 0; k < nk; ++k)
-              mma_i8_pair(d_main, ad + 2 * k, bd + 2 * k, p.idesc_main, (c | k) != 0);
+            const int nk = (p.k_main - c * 128 + 31) / 32;  // K = 32 int8 per MMA
+            if (elect_one()) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                if (k < nk) mma_i8_pair(d_main, ad + 2 * k, bd + 2 * k, p.idesc_main, (c | k) != 0);
+              tc_commit_pair(&empty[stage]);
+            }
           }
-          tc_commit_pair(&empty[stage]);
-          if (++stage == G2_STAGES) { stage = 0; phase ^= 1; }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        tc_commit_pair(&tfull[b]);
+        if (elect_one()) tc_commit_pair(&tfull[b]);
+        __syncwarp();
       }
     }
   } else {
@@ -260,7 +295,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
         if (p.row_zp) zp = p.row_zp[row];
         if (has_aux && p.row_rho) rho = p.row_rho[row];
       }
-      const uint32_t lane_base = tmem + ((uint32_t)(lq * 32) << 16) + b * 256;
+      const uint32_t lane_base = tmem + ((uint32_t)(lq * 32) << 16) + b * (has_aux ? 256 : p.bn);
       for (int c0 = 0; c0 < p.bn; c0 += 32) {
         uint32_t am[32], af[32];
         tmem_ld32(lane_base + c0, am);

@@ -486,7 +486,11 @@ bool map_f16(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64
                      64);
 }
 
-int tile_n(int64_t n) { return (int)std::min<int64_t>(G2_BN, round_up(n, 32)); }
+// tile N: up to 128 with the fp32 aux accumulator (two buffers of main + aux),
+// up to 256 without it (two buffers of main)
+int tile_n(int64_t n, bool aux) {
+  return (int)std::min<int64_t>(aux ? G2_BN : G2_BN_MAX, round_up(n, 32));
+}
 
 // i8 MMA instruction descriptor for the pair (M = 256), f16 likewise
 uint32_t idesc_i8(bool a_signed, int bn) { return make_idesc(2, a_signed ? 1u : 0u, 1, G2_BM, bn); }
@@ -666,7 +670,7 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
     g.p.M = (int)T;
     g.p.m_count = m_count;
     g.p.N = (int)r;
-    g.p.bn = tile_n(r);
+    g.p.bn = tile_n(r, false);
     g.p.k_main = (int)L->n_main;
     g.p.idesc_main = idesc_i8(a_signed, g.p.bn);
     g.p.mode = G2_LR1;
@@ -701,7 +705,7 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   GemmLaunch g{};
   g.p.M = (int)T;
   g.p.N = (int)L->d_out;
-  g.p.bn = tile_n(L->d_out);
+  g.p.bn = tile_n(L->d_out, L->k_lr > 0);
   g.p.k_main = (int)L->n_main;
   g.p.k_aux = (int)L->k_lr;
   g.p.idesc_main = idesc_i8(L->act.centered, g.p.bn);
@@ -805,7 +809,7 @@ int splitq_gemm_i8(const int8_t* a, int64_t lda, int a_signed, const int8_t* b, 
   GemmLaunch g{};
   g.p.M = (int)m;
   g.p.N = (int)n;
-  g.p.bn = tile_n(n);
+  g.p.bn = tile_n(n, false);
   g.p.k_main = (int)k;
   g.p.idesc_main = idesc_i8(a_signed != 0, g.p.bn);
   g.p.mode = G2_RAW;
