@@ -481,6 +481,73 @@ __device__ void outlier_codes(const K1Params& p, int row, const T* xs, const int
   }
 }
 
+
+// raw-bit finiteness test per input type: max of |bits| >= inf pattern
+template <typename T> struct InBits;
+template <> struct InBits<__half> {
+  static constexpr uint32_t inf = 0x7C00u;
+  static __device__ __forceinline__ uint32_t absbits(__half v) { return __half_as_ushort(v) & 0x7FFFu; }
+};
+template <> struct InBits<__nv_bfloat16> {
+  static constexpr uint32_t inf = 0x7F80u;
+  static __device__ __forceinline__ uint32_t absbits(__nv_bfloat16 v) {
+    return __bfloat16_as_ushort(v) & 0x7FFFu;
+  }
+};
+template <> struct InBits<float> {
+  static constexpr uint32_t inf = 0x7F800000u;
+  static __device__ __forceinline__ uint32_t absbits(float v) { return __float_as_uint(v) & 0x7FFFFFFFu; }
+};
+template <> struct InBits<double> {
+  static constexpr uint32_t inf = 0x7FF00000u;
+  static __device__ __forceinline__ uint32_t absbits(double v) {
+    return (uint32_t)__double2hiint(v) & 0x7FFFFFFFu;
+  }
+};
+
+// 4 main elements k0..k0+3 from the staged row; the gather tables are padded
+// to ld_main with (index 0, scale NaN), so no bounds checks. Without a gather
+// (quantize_rows) elements past n_main become NaN.
+template <typename T, bool GATHER>
+__device__ __forceinline__ void gather4_pad(const K1Params& p, const T* xs, int k0,
+                                            double (&z)[4], uint32_t& xbits) {
+  if (GATHER) {
+    const int4 c4 = __ldg(reinterpret_cast<const int4*>(p.c_main + k0));
+    const double2 d0 = __ldg(reinterpret_cast<const double2*>(p.d_main + k0));
+    const double2 d1 = __ldg(reinterpret_cast<const double2*>(p.d_main + k0 + 2));
+    const int c[4] = {c4.x, c4.y, c4.z, c4.w};
+    const double d[4] = {d0.x, d0.y, d1.x, d1.y};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const T xv = xs[c[u]];
+      xbits = max(xbits, InBits<T>::absbits(xv));
+      z[u] = __dmul_rn(to_f64(xv), d[u]);
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool in = k0 + u < p.n_main;
+      const T xv = xs[in ? k0 + u : 0];
+      xbits = max(xbits, in ? InBits<T>::absbits(xv) : 0u);
+      z[u] = in ? to_f64(xv) : __longlong_as_double(0x7ff8000000000000ll);
+    }
+  }
+}
+
+// OR of a per-thread flag over the row group (red: >= 2 * G doubles of scratch)
+template <int G>
+__device__ __forceinline__ bool group_any_flag(bool v, double* red, int g, int wg) {
+  v = __any_sync(0xffffffffu, v);
+  if (G == 1) return v;
+  if ((threadIdx.x & 31) == 0) red[2 * wg] = v ? 1.0 : 0.0;
+  group_sync<G>(g);
+  double any = 0.0;
+#pragma unroll
+  for (int w = 0; w < G; ++w) any += red[2 * w];
+  group_sync<G>(g);
+  return any != 0.0;
+}
+
 // One row per group of G warps (K1G_WARPS / G rows per CTA). The row is
 // staged into SMEM with one TMA bulk copy (cp.async.bulk) when it is 16-B
 // aligned, then every pass gathers from SMEM.
@@ -526,22 +593,20 @@ __global__ void __launch_bounds__(K1G_WARPS * 32) k1_group_kernel(const K1Params
     group_sync<G>(g);
   }
 
-  // ---- pass 1: row min / max of z = x * d
+  // ---- pass 1: row min / max of z = x * d. Padded table entries (scale NaN)
+  // never win a comparison; finiteness is checked on the raw input bits.
   double lo = INFINITY, hi = -INFINITY;
-  bool nan = false;
-  for (int k0 = 4 * tg; k0 < n_main; k0 += 4 * NTG) {
+  uint32_t xbits = 0;
+  for (int k0 = 4 * tg; k0 < ld; k0 += 4 * NTG) {
     double z[4];
-    gather4_smem<T, GATHER>(p, xs, k0, k0 + 3 < n_main, z);
+    gather4_pad<T, GATHER>(p, xs, k0, z, xbits);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      nan |= z[u] != z[u];
-      if (k0 + u < n_main) {
-        lo = z[u] < lo ? z[u] : lo;
-        hi = z[u] > hi ? z[u] : hi;
-      }
+      lo = z[u] < lo ? z[u] : lo;
+      hi = z[u] > hi ? z[u] : hi;
     }
   }
-  nan = __any_sync(0xffffffffu, nan);
+  bool nan = __any_sync(0xffffffffu, xbits >= InBits<T>::inf);
   if (G > 1) {
     if (lane == 0) red[2 * wg] = nan ? 1.0 : 0.0;
     group_sync<G>(g);
@@ -626,29 +691,34 @@ __global__ void __launch_bounds__(K1G_WARPS * 32) k1_group_kernel(const K1Params
   double elo = INFINITY, ehi = -INFINITY;
   for (int k0 = 4 * tg; k0 < ld; k0 += 4 * NTG) {
     double z[4];
-    gather4_smem<T, GATHER>(p, xs, k0, k0 + 3 < n_main, z);
-    int q[4];
-    bool tie = false;
+    uint32_t dummy = 0;
+    gather4_pad<T, GATHER>(p, xs, k0, z, dummy);
+    int qv[4];
+    bool t4[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) q[u] = quant_row(z[u], rp, tie);
-    if (tie) {
+    for (int u = 0; u < 4; ++u) {
+      t4[u] = false;
+      qv[u] = quant_row(z[u], rp, t4[u]);
+    }
+    if (t4[0] | t4[1] | t4[2] | t4[3]) {  // exact .5 ties are common with fp16 inputs
 #pragma unroll
-      for (int u = 0; u < 4; ++u) q[u] = quant_exact(z[u], rp.S, 0.0, rp.zp, rp.qmin, rp.qmax);
+      for (int u = 0; u < 4; ++u)
+        if (t4[u]) qv[u] = quant_exact(z[u], rp.S, 0.0, rp.zp, rp.qmin, rp.qmax);
     }
     uint32_t packed = 0;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
+      const int q = qv[u];
       const bool in = k0 + u < n_main;
-      packed |= (uint32_t)((in ? (cen ? q[u] - rp.zp : q[u]) : 0) & 0xFF) << (8 * u);
-      if (mac && in) {
-        const double e = __dsub_rn(z[u], xh[q[u] - rp.qmin]);
+      packed |= (uint32_t)((in ? (cen ? q - rp.zp : q) : 0) & 0xFF) << (8 * u);
+      if (mac) {  // padded elements give e = NaN, which never wins
+        const double e = __dsub_rn(z[u], xh[q - rp.qmin]);
         elo = e < elo ? e : elo;
         ehi = e > ehi ? e : ehi;
       }
     }
     *reinterpret_cast<uint32_t*>(arow + k0) = packed;
   }
-
   // ---- clear the low-rank columns of the auxiliary operand row (LR1 fills them)
   if (p.k_lr > 0) {
     uint4* lr = reinterpret_cast<uint4*>(p.lr_a + (int64_t)row * p.k_lr + p.lr_off_s);
@@ -671,21 +741,24 @@ __global__ void __launch_bounds__(K1G_WARPS * 32) k1_group_kernel(const K1Params
   int8_t* erow = p.a_mac + (int64_t)cix * ld;
   for (int k0 = 4 * tg; k0 < ld; k0 += 4 * NTG) {
     double z[4];
-    gather4_smem<T, GATHER>(p, xs, k0, k0 + 3 < n_main, z);
+    uint32_t dummy = 0;
+    gather4_pad<T, GATHER>(p, xs, k0, z, dummy);
     const uint32_t codes = *reinterpret_cast<const uint32_t*>(arow + k0);
     double e[4];
     int qe[4];
-    bool tie = false;
+    bool t4[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int c = cen ? (int)(int8_t)(codes >> (8 * u)) : (int)((codes >> (8 * u)) & 0xFF);
       const int q = cen ? c + rp.zp : c;
       e[u] = __dsub_rn(z[u], xh[min(max(q, rp.qmin), rp.qmax) - rp.qmin]);
-      qe[u] = quant_row(e[u], re, tie);
+      t4[u] = false;
+      qe[u] = quant_row(e[u], re, t4[u]);
     }
-    if (tie) {
+    if (t4[0] | t4[1] | t4[2] | t4[3]) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) qe[u] = quant_exact(e[u], re.S, 0.0, re.zp, re.qmin, re.qmax);
+      for (int u = 0; u < 4; ++u)
+        if (t4[u]) qe[u] = quant_exact(e[u], re.S, 0.0, re.zp, re.qmin, re.qmax);
     }
     uint32_t packed = 0;
 #pragma unroll

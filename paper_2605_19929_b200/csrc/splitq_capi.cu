@@ -282,10 +282,15 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
   {
     auto cm = to_i32(d->c_main, d->n_main), ct = to_i32(d->c_text, d->n_text),
          cv = to_i32(d->c_vision, d->n_vision);
+    // main gather tables padded to ld_main with (index 0, scale NaN): K1 reads
+    // whole 4-element groups without bounds checks (quantize_fast.cuh)
+    cm.resize((size_t)L->ld_main, 0);
+    std::vector<double> dm(d->scale_main, d->scale_main + d->n_main);
+    dm.resize((size_t)L->ld_main, std::nan(""));
     if ((rc = L->mem.upload(&L->c_main, cm.data(), cm.size()))) return cleanup(rc);
     if ((rc = L->mem.upload(&L->c_text, ct.data(), ct.size()))) return cleanup(rc);
     if ((rc = L->mem.upload(&L->c_vis, cv.data(), cv.size()))) return cleanup(rc);
-    if ((rc = L->mem.upload(&L->d_main, d->scale_main, d->n_main))) return cleanup(rc);
+    if ((rc = L->mem.upload(&L->d_main, dm.data(), dm.size()))) return cleanup(rc);
     if ((rc = L->mem.upload(&L->d_text, d->scale_text, d->n_text))) return cleanup(rc);
     if ((rc = L->mem.upload(&L->d_vis, d->scale_vision, d->n_vision))) return cleanup(rc);
   }
