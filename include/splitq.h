@@ -162,23 +162,35 @@ int splitq_gemm_i8(const int8_t* a, int64_t lda, int a_signed, const int8_t* b, 
                    int32_t* c, int64_t ldc, int64_t m, int64_t n, int64_t k, void* stream);
 
 /* MOCD calibration statistics (mocd.py:72-150; transform.py:89).
- * x device [tokens x x_ld] (x_dtype), tags device uint8. */
+ * x device [tokens x x_ld] (x_dtype), tags device uint8. All asynchronous. */
+
+/* vision_max[c] = max over vision rows of |x[:, c]| (vision_score,
+ * mocd.py:72-77); all_max[c] = max over all rows (the init_transform
+ * statistic, transform.py:89). fp64 [dim]; status: SPLITQ_STATUS_* bits. */
 int splitq_mocd_absmax(const void* x, int x_dtype, int64_t x_ld, const uint8_t* tags,
-                       int64_t tokens, int64_t dim, float* vision_max, float* all_max,
+                       int64_t tokens, int64_t dim, double* vision_max, double* all_max,
                        int32_t* status, void* stream);
-/* percentile_rank numerators: counts[i][c] = #{j in cand : |x_ij| <= |x_ic|}
- * for the text rows (compact order), uint16 [n_text x n_cand]. */
+/* percentile_rank numerators (mocd.py:92-111): counts[i][j] =
+ * #{l in cand : |x[r_i, l]| <= |x[r_i, cand[j]]|} for the text rows
+ * r_i = text_rows[i], i < *n_text (device count, max_text rows allocated);
+ * uint16 [max_text x n_cand], row-major. */
 int splitq_mocd_rank_counts(const void* x, int x_dtype, int64_t x_ld, const int32_t* text_rows,
                             const int32_t* n_text, int64_t max_text, const int32_t* cand,
                             int64_t n_cand, uint16_t* counts, void* stream);
-/* per-channel histogram of rank counts: hist[c][v] = #{text rows with count v},
- * v in [1, n_cand]; int32 [n_cand x (n_cand + 1)]. Summed across ranks by NCCL. */
-int splitq_mocd_histogram(const uint16_t* counts, const int32_t* n_text, int64_t max_text,
-                          int64_t n_cand, int32_t* hist, void* stream);
-/* text_score from the (all-reduced) histograms: 1-D k-means within-cluster
- * variance per channel (mocd.py:114-150), fp64 [n_cand]. */
-int splitq_mocd_text_score(const int32_t* hist, int64_t n_cand, int64_t n_text, int k,
-                           int max_iter, double* scores, void* stream);
+/* out[c][r] = in[r][c] (uint16), out row stride ld_out. */
+int splitq_mocd_transpose_u16(const uint16_t* in, int64_t rows, int64_t cols, uint16_t* out,
+                              int64_t ld_out, void* stream);
+/* text_score (mocd.py:141-150) for candidate channels [c0, c1): _kmeans_1d
+ * (mocd.py:114-138) of counts_t[c][0..n_text) / n_cand, evaluated with
+ * numpy's exact float64 arithmetic (quantile init, pairwise-sum means).
+ * counts_t: uint16 [n_cand x ld] (transposed counts); scores fp64 [n_cand]. */
+int splitq_mocd_text_score(const uint16_t* counts_t, int64_t ld, int64_t n_cand, int64_t n_text,
+                           int k, int max_iter, int64_t c0, int64_t c1, double* scores,
+                           void* stream);
+/* select_topk (mocd.py:80-89): ascending indices of the k largest scores,
+ * ties to the lower index. flags: int32 [n] scratch, out: int64 [k]. */
+int splitq_mocd_topk(const double* scores, int64_t n, int64_t k, int32_t* flags, int64_t* out,
+                     void* stream);
 
 #ifdef __cplusplus
 }

@@ -184,3 +184,148 @@ def kmeans_1d_hist(hist, n_cand, k, max_iter):
 
 def text_score_hist(hists, n_cand, k, max_iter=50):
     return np.array([kmeans_1d_hist(h, n_cand, k, max_iter) for h in hists])
+
+
+# ---------------------------------------------------------------- exact streaming form
+
+def pairwise_sum(a):
+    """numpy's float64 add.reduce: 8-accumulator pairwise summation
+    (numpy/_core/src/umath/loops_utils.h.src pairwise_sum), verified
+    bit-for-bit against np.sum in tests/test_oracle_golden.py."""
+    def pw(lo, n):
+        if n < 8:
+            res = 0.0
+            for i in range(n):
+                res += a[lo + i]
+            return res
+        if n <= 128:
+            r = [a[lo + j] for j in range(8)]
+            i = 8
+            while i < n - (n % 8):
+                for j in range(8):
+                    r[j] += a[lo + i + j]
+                i += 8
+            res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+            while i < n:
+                res += a[lo + i]
+                i += 1
+            return res
+        n2 = n // 2
+        n2 -= n2 % 8
+        return pw(lo, n2) + pw(lo + n2, n - n2)
+    a = [float(v) for v in a]
+    return pw(0, len(a))
+
+
+def kmeans_1d_exact(counts, n_cand, k, max_iter):
+    """_kmeans_1d (mocd.py:114-138) on one channel's rank counts in token
+    order, written the way the GPU kernel evaluates it: values v = c / n_cand,
+    order statistics from a counting sort, per-level assignment, centre means
+    as numpy pairwise sums over the members in token order. Bit-identical to
+    the reference (checked in tests)."""
+    counts = np.asarray(counts, np.int64)
+    vals = counts / n_cand
+    n = vals.size
+    hist = np.bincount(counts, minlength=n_cand + 1)
+    levels = np.flatnonzero(hist)
+    k = min(k, levels.size)
+    if k == 1:
+        mean = pairwise_sum(vals) / n
+        dev = vals - mean
+        return pairwise_sum(dev * dev) / n
+    cum = np.cumsum(hist)
+
+    def order_stat(idx):
+        return np.searchsorted(cum, idx, side="right") / n_cand
+
+    qs = (2 * np.arange(1, k + 1) - 1) / (2 * k)
+    centers = np.empty(k)
+    for j in range(k):
+        vi = (n - 1) * qs[j]
+        lo = int(np.floor(vi)) if vi < n - 1 else n - 1
+        hi = lo + 1 if vi < n - 1 else n - 1
+        t = vi - np.floor(vi)
+        a, b = order_stat(lo), order_stat(hi)
+        diff = b - a
+        centers[j] = b - diff * (1 - t) if t >= 0.5 else a + diff * t
+
+    def assign_levels(c):
+        lv = levels / n_cand
+        return np.argmin(np.abs(lv[:, None] - c[None, :]), axis=1)
+
+    lvl_of = np.full(n_cand + 1, -1, np.int64)
+    lvl_of[levels] = np.arange(levels.size)
+    assign = assign_levels(centers)
+    for _ in range(max_iter):
+        new_centers = centers.copy()
+        a_tok = assign[lvl_of[counts]]
+        for j in range(k):
+            members = vals[a_tok == j]
+            if members.size:
+                new_centers[j] = pairwise_sum(members) / members.size
+        new_assign = assign_levels(new_centers)
+        centers = new_centers
+        if np.array_equal(new_assign, assign):
+            break
+        assign = new_assign
+    dev = vals - centers[assign[lvl_of[counts]]]
+    return pairwise_sum(dev * dev) / n
+
+
+class PairwiseStream:
+    """numpy's pairwise summation of a stream of known length n, consuming
+    one value at a time (post-order evaluation of the recursion tree:
+    segments > 128 split at n2 = n/2 - (n/2) % 8, leaves of >= 8 elements use
+    8 accumulators, leaves of < 8 a sequential sum from 0.0). This is the
+    exact algorithm of the GPU text-score kernel (csrc/mocd.cu)."""
+
+    def __init__(self, n):
+        self.stack = []  # frames [seg_len, n2, phase, left_sum]
+        self.total = None
+        if n == 0:
+            self.total = 0.0
+            return
+        self._descend(n)
+
+    def _descend(self, m):
+        while m > 128:
+            n2 = m // 2
+            n2 -= n2 % 8
+            self.stack.append([m, n2, 0, 0.0])
+            m = n2
+        self.leaf_len, self.leaf_i = m, 0
+        self.r = [0.0] * 8
+        self.res = 0.0
+
+    def push(self, v):
+        m, i = self.leaf_len, self.leaf_i
+        if m < 8:
+            self.res += v
+        else:
+            body = m - m % 8
+            if i < 8:
+                self.r[i] = v
+            elif i < body:
+                self.r[i % 8] += v
+            else:
+                if i == body:
+                    r = self.r
+                    self.res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+                self.res += v
+            if i == m - 1 and body == m:
+                r = self.r
+                self.res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+        self.leaf_i = i + 1
+        if self.leaf_i == m:
+            self._finish_leaf(self.res)
+
+    def _finish_leaf(self, s):
+        while self.stack:
+            f = self.stack[-1]
+            if f[2] == 0:
+                f[2], f[3] = 1, s
+                self._descend(f[0] - f[1])
+                return
+            s = f[3] + s
+            self.stack.pop()
+        self.total = s

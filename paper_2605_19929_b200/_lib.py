@@ -110,8 +110,10 @@ def load(build_if_missing: bool = True):
         "splitq_mocd_absmax": (C.c_int, [_p, C.c_int, _i64, _p, _i64, _i64, _p, _p, _p, _p]),
         "splitq_mocd_rank_counts": (C.c_int, [_p, C.c_int, _i64, _p, _p, _i64, _p, _i64, _p,
                                               _p]),
-        "splitq_mocd_histogram": (C.c_int, [_p, _p, _i64, _i64, _p, _p]),
-        "splitq_mocd_text_score": (C.c_int, [_p, _i64, _i64, C.c_int, C.c_int, _p, _p]),
+        "splitq_mocd_transpose_u16": (C.c_int, [_p, _i64, _i64, _p, _i64, _p]),
+        "splitq_mocd_text_score": (C.c_int, [_p, _i64, _i64, _i64, C.c_int, C.c_int, _i64, _i64,
+                                             _p, _p]),
+        "splitq_mocd_topk": (C.c_int, [_p, _i64, _i64, _p, _p, _p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -125,8 +127,8 @@ EXPORTED_SYMBOLS = (
     "splitq_last_error", "splitq_version", "splitq_device_sm_count",
     "splitq_layer_create", "splitq_layer_destroy", "splitq_workspace_layout",
     "splitq_forward", "splitq_read_status", "splitq_profile_read", "splitq_quantize_rows", "splitq_gemm_i8",
-    "splitq_mocd_absmax", "splitq_mocd_rank_counts", "splitq_mocd_histogram",
-    "splitq_mocd_text_score",
+    "splitq_mocd_absmax", "splitq_mocd_rank_counts", "splitq_mocd_transpose_u16",
+    "splitq_mocd_text_score", "splitq_mocd_topk",
 )
 
 

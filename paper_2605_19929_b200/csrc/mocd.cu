@@ -1,14 +1,542 @@
-// MOCD calibration statistics (placeholder until the K6 kernels land).
+// MOCD calibration statistics on sm_100a (reference: pkg/src/modquant/mocd.py).
+//
+//   absmax      per-channel max |x| over vision rows (vision_score, mocd.py:72-77)
+//               and over all rows (init_transform statistic, transform.py:89)
+//   rank_counts percentile_rank numerators (mocd.py:92-111): per text row, the
+//               keys |x[row, cand]| are radix-sorted in SMEM and every count is
+//               the upper bound of its own key (ties via <=)
+//   text_score  _kmeans_1d per channel (mocd.py:114-150) evaluated exactly as
+//               numpy does: order statistics from the channel's level histogram,
+//               numpy 'linear' quantile init, per-level nearest-centre
+//               assignment (ties to the lower index), centre means and the final
+//               variance as numpy pairwise sums over the members in token order
+//               (streamed, PairwiseStream below), so scores are bit-identical
+//   topk        select_topk (mocd.py:80-89): k largest, ties to the lower index
+// Multi-GPU (mocd_gpu.py): absmax is MAX-all-reduced, the integer rank counts
+// are all-gathered in token order and channels are sharded for text_score.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cub/block/block_radix_sort.cuh>
+#include <string>
+
 #include "../../include/splitq.h"
+
+namespace {
+
+}  // namespace
+extern "C" int splitq_internal_fail(int code, const char* msg);  // splitq_capi.cu
+namespace {
+
+int mfail(int code, const char* msg) { return splitq_internal_fail(code, msg); }
+
+template <typename T>
+__device__ __forceinline__ double absval(const void* x, int64_t idx) {
+  return fabs((double)reinterpret_cast<const T*>(x)[idx]);
+}
+template <>
+__device__ __forceinline__ double absval<__half>(const void* x, int64_t idx) {
+  return fabs((double)__half2float(reinterpret_cast<const __half*>(x)[idx]));
+}
+template <>
+__device__ __forceinline__ double absval<__nv_bfloat16>(const void* x, int64_t idx) {
+  return fabs((double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(x)[idx]));
+}
+
+// ---------------------------------------------------------------- absmax
+// max over non-negative doubles == max over their bit patterns
+template <typename T>
+__global__ void mocd_absmax_kernel(const void* x, int64_t ld, const uint8_t* tags, int64_t T_,
+                                   int64_t D, int64_t rows_per_block, unsigned long long* vmax,
+                                   unsigned long long* amax, int* status) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= D) return;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block;
+  const int64_t r1 = min(T_, r0 + rows_per_block);
+  double mv = 0.0, ma = 0.0;
+  bool bad = false;
+  for (int64_t r = r0; r < r1; ++r) {
+    const double a = absval<T>(x, r * ld + c);
+    bad |= !(a <= 1.7976931348623157e308);
+    ma = fmax(ma, a);
+    if (tags[r] == 1) mv = fmax(mv, a);
+  }
+  if (bad) atomicOr(status, SPLITQ_STATUS_NONFINITE);
+  atomicMax(&amax[c], (unsigned long long)__double_as_longlong(ma));
+  atomicMax(&vmax[c], (unsigned long long)__double_as_longlong(mv));
+}
+
+__global__ void mocd_tag_check_kernel(const uint8_t* tags, int64_t T_, int* status) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T_;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (tags[i] > 1) atomicOr(status, SPLITQ_STATUS_TAG);
+}
+
+// ---------------------------------------------------------------- rank counts
+template <typename T>
+struct KeyOf {
+  using type = uint32_t;
+  static __device__ __forceinline__ uint32_t get(const void* x, int64_t i) {
+    return __float_as_uint((float)absval<T>(x, i));  // exact for f16 / bf16 / f32
+  }
+};
+template <>
+struct KeyOf<double> {
+  using type = unsigned long long;
+  static __device__ __forceinline__ unsigned long long get(const void* x, int64_t i) {
+    return (unsigned long long)__double_as_longlong(absval<double>(x, i));
+  }
+};
+
+constexpr int RC_THREADS = 256;
+
+template <typename T, int ITEMS>
+__global__ void __launch_bounds__(RC_THREADS) mocd_rank_counts_kernel(
+    const void* x, int64_t ld, const int* text_rows, const int* n_text, const int* cand,
+    int n_cand, uint16_t* counts) {
+  using Key = typename KeyOf<T>::type;
+  using Sort = cub::BlockRadixSort<Key, RC_THREADS, ITEMS>;
+  extern __shared__ __align__(16) uint8_t rc_smem[];
+  typename Sort::TempStorage& tmp = *reinterpret_cast<typename Sort::TempStorage*>(rc_smem);
+  Key* sorted = reinterpret_cast<Key*>(rc_smem + (sizeof(typename Sort::TempStorage) + 15) / 16 * 16);
+  const int i = blockIdx.x;
+  if (i >= *n_text) return;
+  const int64_t xrow = (int64_t)text_rows[i] * ld;
+  Key keys[ITEMS];
+#pragma unroll
+  for (int u = 0; u < ITEMS; ++u) {
+    const int j = threadIdx.x * ITEMS + u;
+    keys[u] = j < n_cand ? KeyOf<T>::get(x, xrow + cand[j]) : (Key)~(Key)0;
+  }
+  Sort(tmp).Sort(keys);
+#pragma unroll
+  for (int u = 0; u < ITEMS; ++u) sorted[threadIdx.x * ITEMS + u] = keys[u];
+  __syncthreads();
+  uint16_t* out = counts + (int64_t)i * n_cand;
+  for (int j = threadIdx.x; j < n_cand; j += RC_THREADS) {
+    const Key v = KeyOf<T>::get(x, xrow + cand[j]);
+    int lo = 0, hi = n_cand;  // first position with sorted > v
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sorted[mid] <= v) lo = mid + 1;
+      else hi = mid;
+    }
+    out[j] = (uint16_t)lo;
+  }
+}
+
+template <typename T, int ITEMS>
+size_t rc_smem_bytes() {
+  using Key = typename KeyOf<T>::type;
+  using Sort = cub::BlockRadixSort<Key, RC_THREADS, ITEMS>;
+  return (sizeof(typename Sort::TempStorage) + 15) / 16 * 16 + sizeof(Key) * RC_THREADS * ITEMS;
+}
+
+template <typename T, int ITEMS>
+int launch_rc(const void* x, int64_t ld, const int* rows, const int* n_text, int64_t max_text,
+              const int* cand, int n_cand, uint16_t* counts, cudaStream_t s) {
+  const size_t smem = rc_smem_bytes<T, ITEMS>();
+  if (smem > 220 * 1024) return mfail(SPLITQ_ERR_UNSUPPORTED, "too many candidate channels");
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(mocd_rank_counts_kernel<T, ITEMS>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return mfail(SPLITQ_ERR_CUDA, "cudaFuncSetAttribute (rank counts)");
+    attr = true;
+  }
+  mocd_rank_counts_kernel<T, ITEMS><<<(unsigned)max_text, RC_THREADS, smem, s>>>(
+      x, ld, rows, n_text, cand, n_cand, counts);
+  return cudaGetLastError() == cudaSuccess ? SPLITQ_OK
+                                           : mfail(SPLITQ_ERR_CUDA, "rank counts launch failed");
+}
+
+template <typename T>
+int launch_rc_items(const void* x, int64_t ld, const int* rows, const int* n_text,
+                    int64_t max_text, const int* cand, int n_cand, uint16_t* counts,
+                    cudaStream_t s) {
+  const int need = (n_cand + RC_THREADS - 1) / RC_THREADS;
+  if (need <= 2) return launch_rc<T, 2>(x, ld, rows, n_text, max_text, cand, n_cand, counts, s);
+  if (need <= 4) return launch_rc<T, 4>(x, ld, rows, n_text, max_text, cand, n_cand, counts, s);
+  if (need <= 8) return launch_rc<T, 8>(x, ld, rows, n_text, max_text, cand, n_cand, counts, s);
+  if (need <= 16) return launch_rc<T, 16>(x, ld, rows, n_text, max_text, cand, n_cand, counts, s);
+  if (need <= 32) return launch_rc<T, 32>(x, ld, rows, n_text, max_text, cand, n_cand, counts, s);
+  if (need <= 48) return launch_rc<T, 48>(x, ld, rows, n_text, max_text, cand, n_cand, counts, s);
+  if (need <= 80) return launch_rc<T, 80>(x, ld, rows, n_text, max_text, cand, n_cand, counts, s);
+  return mfail(SPLITQ_ERR_UNSUPPORTED, "at most 20480 candidate channels");
+}
+
+// ---------------------------------------------------------------- transpose
+__global__ void transpose_u16_kernel(const uint16_t* in, int64_t rows, int64_t cols,
+                                     uint16_t* out, int64_t ld_out) {
+  __shared__ uint16_t tile[32][33];
+  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int64_t r = r0 + dy, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[dy][threadIdx.x] = in[r * cols + c];
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int64_t c = c0 + dy, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[c * ld_out + r] = tile[threadIdx.x][dy];
+  }
+}
+
+// ---------------------------------------------------------------- exact k-means
+// numpy float64 pairwise summation of a stream of known length (see
+// oracle/mocd_oracle.py PairwiseStream for the reference-checked model).
+struct PairwiseStream {
+  int len_[24], n2_[24], phase_[24];
+  double left_[24];
+  int depth;
+  int leaf_len, leaf_i;
+  double r[8];
+  double res;
+  double total;
+  bool done;
+
+  __device__ void init(int n) {
+    depth = 0;
+    done = false;
+    total = 0.0;
+    if (n == 0) {
+      done = true;
+      return;
+    }
+    descend(n);
+  }
+  __device__ void descend(int m) {
+    while (m > 128) {
+      int n2 = m / 2;
+      n2 -= n2 % 8;
+      len_[depth] = m;
+      n2_[depth] = n2;
+      phase_[depth] = 0;
+      left_[depth] = 0.0;
+      ++depth;
+      m = n2;
+    }
+    leaf_len = m;
+    leaf_i = 0;
+    res = 0.0;
+  }
+  __device__ static double combine8(const double* r) {
+    return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  }
+  __device__ void push(double v) {
+    const int m = leaf_len, i = leaf_i;
+    if (m < 8) {
+      res += v;
+    } else {
+      const int body = m - m % 8;
+      if (i < 8) r[i] = v;
+      else if (i < body) r[i & 7] += v;
+      else {
+        if (i == body) res = combine8(r);
+        res += v;
+      }
+      if (i == m - 1 && body == m) res = combine8(r);
+    }
+    leaf_i = i + 1;
+    if (leaf_i == m) finish_leaf(res);
+  }
+  __device__ void finish_leaf(double s) {
+    while (depth > 0) {
+      const int f = depth - 1;
+      if (phase_[f] == 0) {
+        phase_[f] = 1;
+        left_[f] = s;
+        descend(len_[f] - n2_[f]);
+        return;
+      }
+      s = left_[f] + s;
+      --depth;
+    }
+    total = s;
+    done = true;
+  }
+};
+
+constexpr int TS_THREADS = 128;
+constexpr int TS_KMAX = 8;
+
+// One CTA per candidate channel c (c0 + blockIdx.x). counts_t: [n_cand x ld] uint16.
+__global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
+    const uint16_t* counts_t, int64_t ld, int n_cand, int n_text, int k_req, int max_iter, int c0,
+    int c1, double* scores) {
+  extern __shared__ __align__(16) uint8_t ts_smem[];
+  int* hist = reinterpret_cast<int*>(ts_smem);             // [n_cand + 1] -> cumulative
+  int8_t* asg = reinterpret_cast<int8_t*>(hist + n_cand + 1);  // [n_cand + 1] level -> cluster
+  __shared__ double centers[TS_KMAX], new_centers[TS_KMAX];
+  __shared__ int n_j[TS_KMAX];
+  __shared__ int distinct, changed;
+  __shared__ double result;
+  const int c = c0 + blockIdx.x;
+  if (c >= c1) return;
+  const uint16_t* col = counts_t + (int64_t)c * ld;
+  const int tid = threadIdx.x;
+  const double nc = (double)n_cand;
+
+  for (int v = tid; v <= n_cand; v += TS_THREADS) hist[v] = 0;
+  if (tid == 0) distinct = 0;
+  __syncthreads();
+  for (int i = tid; i < n_text; i += TS_THREADS) atomicAdd(&hist[col[i]], 1);
+  __syncthreads();
+  for (int v = tid; v <= n_cand; v += TS_THREADS)
+    if (hist[v]) atomicAdd(&distinct, 1);
+  __syncthreads();
+  // cumulative histogram (one thread; n_cand <= ~20k)
+  if (tid == 0) {
+    int acc = 0;
+    for (int v = 0; v <= n_cand; ++v) {
+      acc += hist[v];
+      hist[v] = acc;
+    }
+  }
+  __syncthreads();
+  const int k = min(k_req, distinct);
+  const int n = n_text;
+
+  if (k <= 1) {
+    // np.var(values): mean = sum / n, then mean((v - mean)^2) (pairwise sums)
+    if (tid == 0) {
+      PairwiseStream ps;
+      ps.init(n);
+      for (int i = 0; i < n; ++i) ps.push((double)col[i] / nc);
+      const double mean = ps.total / (double)n;
+      ps.init(n);
+      for (int i = 0; i < n; ++i) {
+        const double d = (double)col[i] / nc - mean;
+        ps.push(d * d);
+      }
+      scores[c] = ps.total / (double)n;
+    }
+    return;
+  }
+
+  // order statistic: value of the idx-th element of the sorted values
+  auto order_stat = [&](int idx) -> double {
+    int lo = 0, hi = n_cand;  // first level with cum > idx
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (hist[mid] > idx) hi = mid;
+      else lo = mid + 1;
+    }
+    return (double)lo / nc;
+  };
+  if (tid < k) {  // np.quantile(values, (2j - 1) / (2k)), method 'linear'
+    const double q = (double)(2 * (tid + 1) - 1) / (double)(2 * k);
+    const double vi = (double)(n - 1) * q;
+    int lo, hi;
+    if (vi >= (double)(n - 1)) {
+      lo = hi = n - 1;
+    } else {
+      lo = (int)floor(vi);
+      hi = lo + 1;
+    }
+    const double t = vi - floor(vi);
+    const double a = order_stat(lo), b = order_stat(hi);
+    const double diff = b - a;
+    centers[tid] = t >= 0.5 ? b - diff * (1.0 - t) : a + diff * t;
+  }
+  __syncthreads();
+  // level assignment: argmin |v - c_j|, ties to the lower index (np.argmin)
+  auto assign_levels = [&](const double* cen, bool track) {
+    for (int v = tid; v <= n_cand; v += TS_THREADS) {
+      if (hist[v] - (v ? hist[v - 1] : 0) == 0) continue;
+      const double x = (double)v / nc;
+      int best = 0;
+      double bd = fabs(x - cen[0]);
+      for (int j = 1; j < k; ++j) {
+        const double d = fabs(x - cen[j]);
+        if (d < bd) {
+          bd = d;
+          best = j;
+        }
+      }
+      if (track && asg[v] != (int8_t)best) changed = 1;
+      asg[v] = (int8_t)best;
+    }
+  };
+  assign_levels(centers, false);
+  __syncthreads();
+  for (int it = 0; it < max_iter; ++it) {
+    if (tid < k) n_j[tid] = 0;
+    if (tid == 0) changed = 0;
+    __syncthreads();
+    for (int v = tid; v <= n_cand; v += TS_THREADS) {
+      const int h = hist[v] - (v ? hist[v - 1] : 0);
+      if (h) atomicAdd(&n_j[asg[v]], h);
+    }
+    __syncthreads();
+    if (tid < k) {  // members.mean() in token order (numpy pairwise)
+      double cj = centers[tid];
+      if (n_j[tid] > 0) {
+        PairwiseStream ps;
+        ps.init(n_j[tid]);
+        for (int i = 0; i < n; ++i) {
+          const int v = col[i];
+          if (asg[v] == tid) ps.push((double)v / nc);
+        }
+        cj = ps.total / (double)n_j[tid];
+      }
+      new_centers[tid] = cj;
+    }
+    __syncthreads();
+    assign_levels(new_centers, true);
+    if (tid < k) centers[tid] = new_centers[tid];
+    __syncthreads();
+    if (!changed) break;
+  }
+  if (tid == 0) {  // mean((values - centers[assign])^2)
+    PairwiseStream ps;
+    ps.init(n);
+    for (int i = 0; i < n; ++i) {
+      const int v = col[i];
+      const double d = (double)v / nc - centers[asg[v]];
+      ps.push(d * d);
+    }
+    result = ps.total / (double)n;
+    scores[c] = result;
+  }
+}
+
+// ---------------------------------------------------------------- top-k
+// rank_i = #{j: s_j > s_i} + #{j < i: s_j == s_i}; selected iff rank_i < k.
+__global__ void mocd_topk_mark_kernel(const double* s, int n, int k, int* flags) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double si = s[i];
+  int rank = 0;
+  for (int j = 0; j < n; ++j) {
+    const double sj = s[j];
+    rank += (sj > si) || (sj == si && j < i);
+  }
+  flags[i] = rank < k;
+}
+__global__ void mocd_topk_compact_kernel(const int* flags, int n, int64_t* out) {
+  // single block: ascending indices of the selected entries
+  __shared__ int base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+    const int i = c0 + threadIdx.x;
+    const int f = i < n ? flags[i] : 0;
+    const unsigned ballot = __ballot_sync(0xffffffffu, f);
+    __shared__ int warp_tot[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) warp_tot[warp] = __popc(ballot);
+    __syncthreads();
+    int off = base;
+    for (int w = 0; w < warp; ++w) off += warp_tot[w];
+    if (f) out[off + __popc(ballot & ((1u << lane) - 1))] = i;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) base += warp_tot[w];
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
 extern "C" {
-int splitq_mocd_absmax(const void*, int, int64_t, const uint8_t*, int64_t, int64_t, float*, float*,
-                       int32_t*, void*) { return SPLITQ_ERR_UNSUPPORTED; }
-int splitq_mocd_rank_counts(const void*, int, int64_t, const int32_t*, const int32_t*, int64_t,
-                            const int32_t*, int64_t, uint16_t*, void*) { return SPLITQ_ERR_UNSUPPORTED; }
-int splitq_mocd_histogram(const uint16_t*, const int32_t*, int64_t, int64_t, int32_t*, void*) {
-  return SPLITQ_ERR_UNSUPPORTED;
+
+int splitq_mocd_absmax(const void* x, int x_dtype, int64_t x_ld, const uint8_t* tags,
+                       int64_t tokens, int64_t dim, double* vision_max, double* all_max,
+                       int32_t* status, void* stream_) {
+  if (!x || !tags || !vision_max || !all_max || !status)
+    return mfail(SPLITQ_ERR_INVALID, "null argument");
+  if (tokens <= 0 || dim <= 0) return mfail(SPLITQ_ERR_INVALID, "empty batch");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
+  if (cudaMemsetAsync(vision_max, 0, dim * 8, s) != cudaSuccess ||
+      cudaMemsetAsync(all_max, 0, dim * 8, s) != cudaSuccess ||
+      cudaMemsetAsync(status, 0, 4, s) != cudaSuccess)
+    return mfail(SPLITQ_ERR_CUDA, "cudaMemsetAsync failed");
+  const int64_t rows_per_block = 256;
+  dim3 grid((unsigned)((dim + 255) / 256), (unsigned)((tokens + rows_per_block - 1) / rows_per_block));
+  auto vm = reinterpret_cast<unsigned long long*>(vision_max);
+  auto am = reinterpret_cast<unsigned long long*>(all_max);
+  switch (x_dtype) {
+    case SPLITQ_F16:
+      mocd_absmax_kernel<__half><<<grid, 256, 0, s>>>(x, x_ld, tags, tokens, dim, rows_per_block, vm, am, status);
+      break;
+    case SPLITQ_BF16:
+      mocd_absmax_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(x, x_ld, tags, tokens, dim, rows_per_block, vm, am, status);
+      break;
+    case SPLITQ_F32:
+      mocd_absmax_kernel<float><<<grid, 256, 0, s>>>(x, x_ld, tags, tokens, dim, rows_per_block, vm, am, status);
+      break;
+    case SPLITQ_F64:
+      mocd_absmax_kernel<double><<<grid, 256, 0, s>>>(x, x_ld, tags, tokens, dim, rows_per_block, vm, am, status);
+      break;
+    default:
+      return mfail(SPLITQ_ERR_INVALID, "bad x dtype");
+  }
+  mocd_tag_check_kernel<<<64, 256, 0, s>>>(tags, tokens, status);
+  return cudaGetLastError() == cudaSuccess ? SPLITQ_OK : mfail(SPLITQ_ERR_CUDA, "absmax launch failed");
 }
-int splitq_mocd_text_score(const int32_t*, int64_t, int64_t, int, int, double*, void*) {
-  return SPLITQ_ERR_UNSUPPORTED;
+
+int splitq_mocd_rank_counts(const void* x, int x_dtype, int64_t x_ld, const int32_t* text_rows,
+                            const int32_t* n_text, int64_t max_text, const int32_t* cand,
+                            int64_t n_cand, uint16_t* counts, void* stream_) {
+  if (!x || !text_rows || !n_text || !cand || !counts) return mfail(SPLITQ_ERR_INVALID, "null argument");
+  if (n_cand <= 0) return mfail(SPLITQ_ERR_INVALID, "candidate channel set is empty");
+  if (n_cand > 65535) return mfail(SPLITQ_ERR_UNSUPPORTED, "at most 65535 candidate channels");
+  if (max_text <= 0) return SPLITQ_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
+  const int nc = (int)n_cand;
+  switch (x_dtype) {
+    case SPLITQ_F16: return launch_rc_items<__half>(x, x_ld, text_rows, n_text, max_text, cand, nc, counts, s);
+    case SPLITQ_BF16: return launch_rc_items<__nv_bfloat16>(x, x_ld, text_rows, n_text, max_text, cand, nc, counts, s);
+    case SPLITQ_F32: return launch_rc_items<float>(x, x_ld, text_rows, n_text, max_text, cand, nc, counts, s);
+    case SPLITQ_F64: return launch_rc_items<double>(x, x_ld, text_rows, n_text, max_text, cand, nc, counts, s);
+    default: return mfail(SPLITQ_ERR_INVALID, "bad x dtype");
+  }
 }
+
+int splitq_mocd_transpose_u16(const uint16_t* in, int64_t rows, int64_t cols, uint16_t* out,
+                              int64_t ld_out, void* stream_) {
+  if (!in || !out) return mfail(SPLITQ_ERR_INVALID, "null argument");
+  if (rows <= 0 || cols <= 0) return SPLITQ_OK;
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  transpose_u16_kernel<<<grid, dim3(32, 8), 0, reinterpret_cast<cudaStream_t>(stream_)>>>(
+      in, rows, cols, out, ld_out);
+  return cudaGetLastError() == cudaSuccess ? SPLITQ_OK : mfail(SPLITQ_ERR_CUDA, "transpose launch failed");
 }
+
+int splitq_mocd_text_score(const uint16_t* counts_t, int64_t ld, int64_t n_cand, int64_t n_text,
+                           int k, int max_iter, int64_t c0, int64_t c1, double* scores,
+                           void* stream_) {
+  if (!counts_t || !scores) return mfail(SPLITQ_ERR_INVALID, "null argument");
+  if (k < 1) return mfail(SPLITQ_ERR_INVALID, "cluster count must be positive");
+  if (k > n_text) return mfail(SPLITQ_ERR_INVALID, "cluster count exceeds number of text tokens");
+  if (k > TS_KMAX) return mfail(SPLITQ_ERR_UNSUPPORTED, "at most 8 clusters on the GPU path");
+  if (c1 <= c0) return SPLITQ_OK;
+  const size_t smem = (size_t)(n_cand + 1) * 4 + (size_t)(n_cand + 1);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(mocd_text_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024) != cudaSuccess)
+      return mfail(SPLITQ_ERR_CUDA, "cudaFuncSetAttribute (text score)");
+    attr = true;
+  }
+  if (smem > 200 * 1024) return mfail(SPLITQ_ERR_UNSUPPORTED, "too many candidate channels");
+  mocd_text_score_kernel<<<(unsigned)(c1 - c0), TS_THREADS, smem,
+                           reinterpret_cast<cudaStream_t>(stream_)>>>(
+      counts_t, ld, (int)n_cand, (int)n_text, k, max_iter, (int)c0, (int)c1, scores);
+  return cudaGetLastError() == cudaSuccess ? SPLITQ_OK : mfail(SPLITQ_ERR_CUDA, "text score launch failed");
+}
+
+int splitq_mocd_topk(const double* scores, int64_t n, int64_t k, int32_t* flags, int64_t* out,
+                     void* stream_) {
+  if (!scores || !flags || !out) return mfail(SPLITQ_ERR_INVALID, "null argument");
+  if (k > n) return mfail(SPLITQ_ERR_INVALID, "k exceeds score vector length");
+  if (k <= 0 || n <= 0) return SPLITQ_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
+  mocd_topk_mark_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(scores, (int)n, (int)k, flags);
+  mocd_topk_compact_kernel<<<1, 1024, 0, s>>>(flags, (int)n, out);
+  return cudaGetLastError() == cudaSuccess ? SPLITQ_OK : mfail(SPLITQ_ERR_CUDA, "topk launch failed");
+}
+
+}  // extern "C"

@@ -194,6 +194,7 @@ int check_codes(const int8_t* q, int64_t count, const QSpecDev& s, const char* n
 extern "C" {
 
 const char* splitq_last_error(void) { return g_last_error.c_str(); }
+int splitq_internal_fail(int code, const char* msg) { return fail(code, "%s", msg); }
 int splitq_version(void) { return 1; }
 
 int splitq_device_sm_count(int device, int* out) {

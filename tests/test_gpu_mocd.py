@@ -1,0 +1,87 @@
+"""GPU MOCD statistics vs the reference (golden fixtures) and the oracle:
+vision scores and percentile ranks exact, text scores bit-identical,
+partitions identical."""
+
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import mocd_oracle as mo
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _pkg():
+    import paper_2605_19929_b200 as pkg
+    from paper_2605_19929_b200 import mocd_gpu
+    return pkg, mocd_gpu
+
+
+def test_golden_mocd_cases():
+    pkg, mg = _pkg()
+    d = np.load(os.path.join(GOLD, "mocd.npz"))
+    for pre in ("s0_", "s1_", "s2_", "r0_", "r1_", "r2_"):
+        x, tags = d[pre + "x"], d[pre + "tags"]
+        k = int(d[pre + "k"]) if pre + "k" in d else 3
+        ratio = 2 / 64 if pre.startswith("s") else 0.125
+        batch = pkg.ActivationBatch(x, tags)
+        if pre + "vscore" in d:
+            np.testing.assert_array_equal(mg.vision_score(batch), d[pre + "vscore"])
+            cand = np.setdiff1d(np.arange(x.shape[1]), d[pre + "c_vision"])
+            np.testing.assert_array_equal(mg.percentile_rank(batch, cand), d[pre + "ranks"])
+        part = mg.build_partition(batch, pkg.MocdConfig(ratio, ratio, clusters_k=k))
+        np.testing.assert_array_equal(part.c_text, d[pre + "c_text"])
+        np.testing.assert_array_equal(part.c_vision, d[pre + "c_vision"])
+        cand = np.setdiff1d(np.arange(x.shape[1]), part.c_vision)
+        counts = mg._GPU.rank_counts(torch.from_numpy(x).cuda(), torch.from_numpy(tags).cuda(), cand)
+        ts = mg.text_score_counts(counts, cand.size, min(k, int((tags == 0).sum()))).cpu().numpy()
+        np.testing.assert_array_equal(ts, d[pre + "tscore"])
+
+
+@pytest.mark.parametrize("seed,n_text,n_vis,dim,k,dtype", [
+    (0, 300, 100, 96, 3, np.float32), (1, 1000, 200, 257, 3, np.float16),
+    (2, 129, 40, 64, 2, np.float64), (3, 700, 100, 130, 4, np.float32),
+    (4, 64, 64, 40, 1, np.float32), (5, 2000, 500, 512, 3, np.float16)])
+def test_random_batches_bit_exact(seed, n_text, n_vis, dim, k, dtype):
+    pkg, mg = _pkg()
+    rng = np.random.default_rng(seed)
+    x = (rng.standard_normal((n_text + n_vis, dim)) * rng.uniform(0.05, 8, dim)).astype(dtype)
+    if seed % 2:  # exact ties and repeated values in the ranks
+        x[:, ::7] = np.round(x[:, ::7])
+    tags = rng.permutation(np.array([0] * n_text + [1] * n_vis, np.uint8))
+    xd = x.astype(np.float64)
+    np.testing.assert_array_equal(mg._GPU.absmax(torch.from_numpy(x).cuda(),
+                                                 torch.from_numpy(tags).cuda())[0].cpu().numpy(),
+                                  mo.vision_score(xd, tags))
+    cand = np.arange(dim)[rng.random(dim) > 0.1]
+    counts = mg._GPU.rank_counts(torch.from_numpy(x).cuda(), torch.from_numpy(tags).cuda(), cand)
+    np.testing.assert_array_equal(counts.cpu().numpy().astype(np.int64) & 0xFFFF,
+                                  mo.rank_counts(xd, tags, cand))
+    ts = mg.text_score_counts(counts, cand.size, k).cpu().numpy()
+    ref = mo.text_score(mo.percentile_rank(xd, tags, cand), k, 50)
+    np.testing.assert_array_equal(ts, ref)
+    cfg = pkg.MocdConfig(0.05, 0.05, clusters_k=k)
+    part = mg.build_partition(pkg.ActivationBatch(xd, tags), cfg)
+    c_main, c_text, c_vision = mo.build_partition(xd, tags, 0.05, 0.05, k)
+    np.testing.assert_array_equal(part.c_text, c_text)
+    np.testing.assert_array_equal(part.c_vision, c_vision)
+
+
+def test_topk_ties_to_lower_index():
+    _, mg = _pkg()
+    s = torch.tensor([3.0, 1.0, 3.0, 2.0, 3.0], dtype=torch.float64, device="cuda")
+    assert mg._GPU.topk(s, 2).cpu().tolist() == [0, 2]
+    assert mg._GPU.topk(s, 4).cpu().tolist() == [0, 2, 3, 4]
+
+
+def test_errors():
+    pkg, mg = _pkg()
+    b = pkg.ActivationBatch(np.ones((4, 8)), [0, 0, 0, 0])
+    with pytest.raises(ValueError, match="vision"):
+        mg.build_partition(b, pkg.MocdConfig(ratio_vision=0.25, ratio_text=0.0))
+    with pytest.raises(ValueError, match="vision"):
+        mg.vision_score(b)

@@ -42,7 +42,7 @@ def spawn(fn, world=2):
     procs = [ctx.Process(target=_run, args=(r, world, port, fn, q)) for r in range(world)]
     for p in procs:
         p.start()
-    out = dict(q.get(timeout=300) for _ in procs)
+    out = dict(q.get(timeout=120) for _ in procs)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -93,3 +93,63 @@ def test_token_shard_partition_covers_rows():
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             sizes = [h - l for l, h in spans]
             assert max(sizes) - min(sizes) <= 1
+
+
+class OracleStats:
+    """CPU stand-in for the per-shard GPU statistics (test infrastructure)."""
+
+    def absmax(self, x, tags):
+        from oracle import mocd_oracle as mo
+        x = np.asarray(x, np.float64)
+        tags = np.asarray(tags)
+        v = np.max(np.abs(x[tags == 1]), axis=0) if np.any(tags == 1) else np.zeros(x.shape[1])
+        return torch.from_numpy(v), torch.from_numpy(mo.column_absmax(x))
+
+    def rank_counts(self, x, tags, cand):
+        from oracle import mocd_oracle as mo
+        return torch.from_numpy(mo.rank_counts(x, tags, cand).astype(np.int16))
+
+    def text_score(self, counts, n_cand, k, max_iter, c0=0, c1=None):
+        from oracle import mocd_oracle as mo
+        c1 = n_cand if c1 is None else c1
+        cnt = counts.numpy().astype(np.int64) & 0xFFFF
+        out = np.zeros(n_cand)
+        for c in range(c0, c1):
+            out[c] = mo.kmeans_1d_exact(cnt[:, c], n_cand, k, max_iter)
+        return torch.from_numpy(out)
+
+    def topk(self, scores, k):
+        from oracle import mocd_oracle as mo
+        return torch.from_numpy(mo.select_topk(scores.numpy(), k))
+
+
+def _mocd_case():
+    rng = np.random.default_rng(11)
+    n, dim = 90, 40
+    x = rng.standard_normal((n, dim)) * rng.uniform(0.1, 4, dim)
+    x[:, 3] *= 30
+    tags = rng.permutation(np.array([0] * 60 + [1] * 30, np.uint8))
+    x[tags == 1, 7] *= 50
+    return x, tags
+
+
+def _sharded_partition(rank, world):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2605_19929_b200 import mocd_gpu, parallel
+    from paper_2605_19929_b200.mocd import MocdConfig
+    x, tags = _mocd_case()
+    lo, hi = parallel.token_shard(x.shape[0], rank, world)
+    p = mocd_gpu.build_partition_distributed(x[lo:hi], tags[lo:hi],
+                                             MocdConfig(0.1, 0.1, clusters_k=3),
+                                             stats=OracleStats())
+    return p.c_main, p.c_text, p.c_vision
+
+
+def test_mocd_partition_distributed_equals_single_process():
+    from oracle import mocd_oracle as mo
+    x, tags = _mocd_case()
+    ref = mo.build_partition(x, tags, 0.1, 0.1, 3)
+    for out in spawn(_sharded_partition):
+        for a, b in zip(out, ref):
+            np.testing.assert_array_equal(a, b)
