@@ -104,7 +104,9 @@ typedef struct {
   int64_t total_bytes;
   int64_t status;                                  /* int32 error word */
   int64_t text_idx, text_rows, n_text;             /* int32 */
-  int64_t a_main; int64_t ld_main;                 /* int8 codes [T x ld_main] */
+  int64_t a_main; int64_t ld_main;                 /* int8 codes [T x ld_main]; column c is
+                                                      channel c when main_natural (outlier
+                                                      columns hold don't-care codes) */
   int64_t s_main, sf_main, zp_main, lrs_main, rho; /* f64, f32, i32, f32, f32 per row */
   int64_t a_text; int64_t ld_text;
   int64_t s_text, sf_text, zp_text;
@@ -115,6 +117,8 @@ typedef struct {
   int64_t lr_a; int64_t k_lr;                      /* fp16 [T x k_lr] low-rank operand */
   int32_t code_centered_main;                      /* 1: codes stored as (q - zp) s8; 0: q as u8 */
   int32_t code_centered_aux;
+  int32_t main_natural;                            /* 1: main / MAC codes in natural channel order */
+  int32_t reserved;
 } splitq_ws_layout_t;
 
 const char* splitq_last_error(void);

@@ -15,7 +15,7 @@ CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_NAME = "libsplitq_b200.so"
 LIB_PATH = os.path.join(PKG_DIR, LIB_NAME)
 SOURCES = ["splitq_capi.cu", "mocd.cu"]
-HEADERS = ["gemm_sm100.cuh", "quantize.cuh", "quantize_fast.cuh", "sm100_ptx.cuh", "tma_host.cuh", "mocd.cuh"]
+HEADERS = ["gemm_sm100.cuh", "quantize.cuh", "quantize_fast.cuh", "sm100_ptx.cuh", "tma_host.cuh", "mocd.cuh", "k1w.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -49,7 +49,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         "-o", LIB_PATH + ".tmp",
         *[os.path.join(CSRC, s) for s in SOURCES],
         "-lcudart",
-    ]
+    ] + os.environ.get("SPLITQ_NVCC_EXTRA", "").split()
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

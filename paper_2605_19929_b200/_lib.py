@@ -64,7 +64,8 @@ class WsLayout(C.Structure):
         "a_vision", "ld_vision", "s_vision", "sf_vision", "zp_vision",
         "a_mac", "s_mac", "zp_mac", "lrs_mac",
         "lr_a", "k_lr",
-    )] + [("code_centered_main", _i32), ("code_centered_aux", _i32)]
+    )] + [("code_centered_main", _i32), ("code_centered_aux", _i32), ("main_natural", _i32),
+          ("reserved", _i32)]
 
 
 class SplitqError(RuntimeError):

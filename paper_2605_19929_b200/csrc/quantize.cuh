@@ -162,6 +162,8 @@ struct K1Params {
   // main path
   const int* c_main;
   const double* d_main;
+  const float* d_main32;  // fp32 copy of d_main (K1 v3)
+  const uint8_t* tags;    // modality tags (K1 v3 validates them)
   int n_main;
   int ld_main;  // row stride (bytes) of the main / MAC code matrices
   QSpecDev act, aux;

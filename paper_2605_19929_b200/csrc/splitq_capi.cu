@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -17,6 +18,7 @@
 #include "gemm2_sm100.cuh"
 #include "quantize.cuh"
 #include "quantize_fast.cuh"
+#include "k1w.cuh"
 #include "tma_host.cuh"
 
 using namespace splitq;
@@ -111,14 +113,17 @@ struct DevBuf {
 };
 
 // K x N row-major centred codes -> N x ld K-major (zero padded) + column sums.
+// With a row map, code row k lands at K position kmap[k] (the natural channel
+// index of main channel k; the other positions stay zero).
 void transpose_codes(const int8_t* q, int64_t K, int64_t N, int64_t ld, std::vector<int8_t>& out,
-                     std::vector<int32_t>& colsum) {
+                     std::vector<int32_t>& colsum, const int64_t* kmap = nullptr) {
   out.assign((size_t)N * ld, 0);
   colsum.assign((size_t)N, 0);
   for (int64_t k = 0; k < K; ++k) {
     const int8_t* src = q + k * N;
+    const int64_t kk = kmap ? kmap[k] : k;
     for (int64_t n = 0; n < N; ++n) {
-      out[(size_t)n * ld + k] = src[n];
+      out[(size_t)n * ld + kk] = src[n];
       colsum[n] += src[n];
     }
   }
@@ -137,11 +142,16 @@ struct splitq_layer_s {
   int64_t d_in = 0, d_out = 0, n_main = 0, n_text = 0, n_vis = 0, r_s = 0, r_c = 0;
   QSpecDev act{}, aux{};
   int use_cws = 0, use_mac = 0;
+  // Main-path codes live in natural channel order: column c of the code rows
+  // is channel c (outlier channels carry don't-care codes against all-zero
+  // weight rows), so K1 needs no gather and the GEMM K is d_in.
+  int64_t k_nat = 0;
   int64_t ld_main = 0, ld_text = 0, ld_vis = 0;
   int64_t r_s16 = 0, r_c16 = 0, k_lr = 0;  // k_lr = K of the fp16 auxiliary GEMM
   int64_t kt16 = 0, kv16 = 0, off_t = 0, off_v = 0, off_s = 0, off_c = 0;
   DevBuf mem;
-  int* c_main = nullptr; double* d_main = nullptr;
+  int* c_main = nullptr; double* d_main = nullptr; float* d_main32 = nullptr;
+  int k3_ok = 0;  // smoothing scales within the fp32 fast path's range
   int* c_text = nullptr; double* d_text = nullptr;
   int* c_vis = nullptr; double* d_vis = nullptr;
   int8_t* b_main = nullptr; float* s_main = nullptr; int* cs_main = nullptr;
@@ -157,10 +167,10 @@ namespace {
 
 int pack_weight(splitq_layer_s* L, const int8_t* q, const double* s, int64_t K, int64_t N,
                 int64_t ld, int8_t** b, float** sc, int** cs, double extra_div = 1.0,
-                const std::vector<double>* per_col_div = nullptr) {
+                const std::vector<double>* per_col_div = nullptr, const int64_t* kmap = nullptr) {
   std::vector<int8_t> t;
   std::vector<int32_t> colsum;
-  transpose_codes(q, K, N, ld, t, colsum);
+  transpose_codes(q, K, N, ld, t, colsum, kmap);
   std::vector<float> sf((size_t)N);
   for (int64_t n = 0; n < N; ++n) {
     double v = s[n] / extra_div;
@@ -256,7 +266,8 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
   L->use_mac = d->use_mac ? 1 : 0;
   L->r_s = L->use_cws ? d->r_cws : 0;
   L->r_c = L->use_mac ? d->r_mac : 0;
-  L->ld_main = round_up(L->n_main, 16);
+  L->k_nat = L->d_in;
+  L->ld_main = round_up(L->d_in, 16);
   L->ld_text = round_up(std::max<int64_t>(L->n_text, 1), 16);
   L->ld_vis = round_up(std::max<int64_t>(L->n_vis, 1), 16);
   L->r_s16 = round_up(L->r_s, 16);
@@ -281,13 +292,21 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
     return v;
   };
   {
-    auto cm = to_i32(d->c_main, d->n_main), ct = to_i32(d->c_text, d->n_text),
-         cv = to_i32(d->c_vision, d->n_vision);
-    // main gather tables padded to ld_main with (index 0, scale NaN): K1 reads
-    // whole 4-element groups without bounds checks (quantize_fast.cuh)
-    cm.resize((size_t)L->ld_main, 0);
-    std::vector<double> dm(d->scale_main, d->scale_main + d->n_main);
-    dm.resize((size_t)L->ld_main, std::nan(""));
+    auto ct = to_i32(d->c_text, d->n_text), cv = to_i32(d->c_vision, d->n_vision);
+    // main tables in natural channel order, padded to ld_main: index c -> c
+    // (padding -> 0) and the smoothing scale of main channel c, NaN for
+    // outlier channels and padding (NaN never wins a min / max, so K1 reads
+    // whole groups without masks; quantize_fast.cuh, k1v3.cuh)
+    std::vector<int32_t> cm((size_t)L->ld_main, 0);
+    for (int64_t c = 0; c < L->d_in; ++c) cm[c] = (int32_t)c;
+    std::vector<double> dm((size_t)L->ld_main, std::nan(""));
+    for (int64_t k = 0; k < d->n_main; ++k) dm[d->c_main[k]] = d->scale_main[k];
+    std::vector<float> dm32((size_t)L->ld_main, std::nanf(""));
+    for (int64_t c = 0; c < L->ld_main; ++c) dm32[c] = (float)dm[c];
+    L->k3_ok = 1;
+    for (int64_t k = 0; k < d->n_main; ++k)
+      if (!(d->scale_main[k] > 1e-30 && d->scale_main[k] < 1e30)) L->k3_ok = 0;
+    if ((rc = L->mem.upload(&L->d_main32, dm32.data(), dm32.size()))) return cleanup(rc);
     if ((rc = L->mem.upload(&L->c_main, cm.data(), cm.size()))) return cleanup(rc);
     if ((rc = L->mem.upload(&L->c_text, ct.data(), ct.size()))) return cleanup(rc);
     if ((rc = L->mem.upload(&L->c_vis, cv.data(), cv.size()))) return cleanup(rc);
@@ -297,7 +316,7 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
   }
   const int64_t N = d->d_out;
   if ((rc = pack_weight(L, d->q_main, d->s_main, d->n_main, N, L->ld_main, &L->b_main, &L->s_main,
-                        &L->cs_main)))
+                        &L->cs_main, 1.0, nullptr, d->c_main)))
     return cleanup(rc);
   if (L->k_lr) {
     // Low-rank first stage: A_lr[i, c] = (S_a[i] / rho_i) * (S_u[c] / sigma_c) * acc[i, c]
@@ -324,7 +343,7 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
         return cleanup(rc);
       sig_s = sigmas(d->q_us, d->s_us, L->r_s, act);
       if ((rc = pack_weight(L, d->q_us, d->s_us, K, L->r_s, L->ld_main, &L->b_us, &L->s_us,
-                            &L->cs_us, 1.0, &sig_s)))
+                            &L->cs_us, 1.0, &sig_s, d->c_main)))
         return cleanup(rc);
     }
     if (L->r_c) {
@@ -333,7 +352,7 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
         return cleanup(rc);
       sig_c = sigmas(d->q_uc, d->s_uc, L->r_c, aux);
       if ((rc = pack_weight(L, d->q_uc, d->s_uc, K, L->r_c, L->ld_main, &L->b_uc, &L->s_uc,
-                            &L->cs_uc, 1.0, &sig_c)))
+                            &L->cs_uc, 1.0, &sig_c, d->c_main)))
         return cleanup(rc);
     }
     // B_aux (fp16, d_out x k_lr, K-major), per column j with colf = S_vs[j]
@@ -448,6 +467,7 @@ int splitq_workspace_layout(splitq_layer_t L, int64_t T, splitq_ws_layout_t* o) 
   if (L->k_lr) o->lr_a = take(2 * T * L->k_lr);
   o->total_bytes = off;
   o->code_centered_main = L->act.centered;
+  o->main_natural = 1;
   o->code_centered_aux = L->aux.centered;
   return SPLITQ_OK;
 }
@@ -548,12 +568,37 @@ int launch_k1_dt(const K1Params& k, int d_in, cudaStream_t s) {
   }
 }
 
+// K1 warp-per-row (fp16 / bf16 rows, d_in % 8 == 0, 16-B aligned rows):
+// fp32 fast path with certified exact fp64 fallback (k1w.cuh).
+template <typename T>
+int launch_k1w(const K1Params& k, int d_in, int device, cudaStream_t stream) {
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1w_kernel<T>, KW_THREADS, 0));
+  if (per_sm < 1) return SPLITQ_ERR_UNSUPPORTED;
+  const int64_t warps = (int64_t)per_sm * sm_count(device) * (KW_THREADS / 32);
+  const int64_t grid = (std::min<int64_t>(k.T, warps) + KW_THREADS / 32 - 1) / (KW_THREADS / 32);
+  k1w_kernel<T><<<(unsigned)grid, KW_THREADS, 0, stream>>>(k, d_in);
+  CUDA_TRY(cudaGetLastError());
+  return SPLITQ_OK;
+}
+
+bool k1v3_eligible(const K1Params& k, int d_in) {
+  if (k.x_dtype != IN_F16 && k.x_dtype != IN_BF16) return false;
+  if (d_in % 8 || (k.ldx % 8) || (reinterpret_cast<uintptr_t>(k.x) & 15)) return false;
+  if (!k.d_main32 || !k.c_main || (k.ld_main % 8) || k.n_main != d_in) return false;
+  return true;
+}
+
 // K1 dispatch: the SMEM-staged row-group kernel; the generic per-row CTA
 // kernel (same arithmetic) covers code strides that are not 16-B multiples
 // and rows too large to stage.
 int launch_k1(const K1Params& k, int d_in, int device, cudaStream_t stream) {
-  (void)device;
   int rc = SPLITQ_ERR_UNSUPPORTED;
+  if (k1v3_eligible(k, d_in) && !getenv("SPLITQ_K1_LEGACY")) {
+    rc = k.x_dtype == IN_F16 ? launch_k1w<__half>(k, d_in, device, stream)
+                             : launch_k1w<__nv_bfloat16>(k, d_in, device, stream);
+    if (rc != SPLITQ_ERR_UNSUPPORTED) return rc;
+  }
   if ((k.ld_main & 15) == 0) {
     rc = (k.c_main && k.d_main) ? launch_k1_dt<true>(k, d_in, stream)
                                 : launch_k1_dt<false>(k, d_in, stream);
@@ -623,7 +668,9 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   k.T = (int)T;
   k.c_main = L->c_main;
   k.d_main = L->d_main;
-  k.n_main = (int)L->n_main;
+  k.d_main32 = L->k3_ok ? L->d_main32 : nullptr;
+  k.tags = tags;
+  k.n_main = (int)L->k_nat;
   k.ld_main = (int)L->ld_main;
   k.act = L->act;
   k.aux = L->aux;
@@ -677,7 +724,7 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
     g.p.m_count = m_count;
     g.p.N = (int)r;
     g.p.bn = tile_n(r, false);
-    g.p.k_main = (int)L->n_main;
+    g.p.k_main = (int)L->k_nat;
     g.p.idesc_main = idesc_i8(a_signed, g.p.bn);
     g.p.mode = G2_LR1;
     g.p.row_s = row_s;
@@ -689,8 +736,8 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
     g.p.col_off = (int)col_off;
     g.p.row_map = row_map;
     g.p.err = err;
-    bool ok = map_i8(&g.maps.a, a_codes, T, L->n_main, L->ld_main, 128) &&
-              map_i8(&g.maps.b, bu, r, L->n_main, L->ld_main, g.p.bn / 2);
+    bool ok = map_i8(&g.maps.a, a_codes, T, L->k_nat, L->ld_main, 128) &&
+              map_i8(&g.maps.b, bu, r, L->k_nat, L->ld_main, g.p.bn / 2);
     g.maps.xa = g.maps.xb = g.maps.a;
     if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (LR1)");
     return launch_gemm(g, L->device, T, stream);
@@ -712,7 +759,7 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   g.p.M = (int)T;
   g.p.N = (int)L->d_out;
   g.p.bn = tile_n(L->d_out, L->k_lr > 0);
-  g.p.k_main = (int)L->n_main;
+  g.p.k_main = (int)L->k_nat;
   g.p.k_aux = (int)L->k_lr;
   g.p.idesc_main = idesc_i8(L->act.centered, g.p.bn);
   g.p.idesc_aux = idesc_f16(g.p.bn);
@@ -727,8 +774,8 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   g.p.out = y;
   g.p.ldo = y_ld;
   if (raw) g.p.raw_aux = reinterpret_cast<float*>(reinterpret_cast<int*>(y) + T * y_ld);
-  bool ok = map_i8(&g.maps.a, at(W.a_main), T, L->n_main, L->ld_main, 128) &&
-            map_i8(&g.maps.b, L->b_main, L->d_out, L->n_main, L->ld_main, g.p.bn / 2);
+  bool ok = map_i8(&g.maps.a, at(W.a_main), T, L->k_nat, L->ld_main, 128) &&
+            map_i8(&g.maps.b, L->b_main, L->d_out, L->k_nat, L->ld_main, g.p.bn / 2);
   g.maps.xa = g.maps.xb = g.maps.a;
   if (ok && L->k_lr)
     ok = map_f16(&g.maps.xa, lr_a, T, L->k_lr, L->k_lr, 128) &&

@@ -64,15 +64,18 @@ def _check_codes(layer, x, tags):
     T = x.shape[0]
     cen_m, cen_a = lay.code_centered_main, lay.code_centered_aux
 
-    def codes_of(off, ld, rows, cols, centered, zp):
-        c = _ws_view(ws, off, np.int8, rows * ld).reshape(rows, ld)[:, :cols].astype(np.int64)
+    def codes_of(off, ld, rows, cols, centered, zp, main=False):
+        c = _ws_view(ws, off, np.int8, rows * ld).reshape(rows, ld)
+        if main and lay.main_natural:  # natural channel order -> the reference's C_m order
+            c = c[:, np.asarray(layer.partition.c_main)]
+        c = c[:, :cols].astype(np.int64)
         return c + zp[:, None] if centered else (c & 0xFF)
 
     q, s, z = act["main"]
     zp = _ws_view(ws, lay.zp_main, np.int32, T).astype(np.int64)
     np.testing.assert_array_equal(zp, z)
     np.testing.assert_array_equal(_ws_view(ws, lay.s_main, np.float64, T), s)
-    np.testing.assert_array_equal(codes_of(lay.a_main, lay.ld_main, T, q.shape[1], cen_m, zp), q)
+    np.testing.assert_array_equal(codes_of(lay.a_main, lay.ld_main, T, q.shape[1], cen_m, zp, main=True), q)
     for name, off_a, off_s, off_z, ld in (("text", lay.a_text, lay.s_text, lay.zp_text, lay.ld_text),
                                           ("vision", lay.a_vision, lay.s_vision, lay.zp_vision,
                                            lay.ld_vision)):
@@ -91,7 +94,7 @@ def _check_codes(layer, x, tags):
         zp = _ws_view(ws, lay.zp_mac, np.int32, n).astype(np.int64)
         np.testing.assert_array_equal(zp, z)
         np.testing.assert_array_equal(_ws_view(ws, lay.s_mac, np.float64, n), s)
-        np.testing.assert_array_equal(codes_of(lay.a_mac, lay.ld_main, n, q.shape[1], cen_a, zp), q)
+        np.testing.assert_array_equal(codes_of(lay.a_mac, lay.ld_main, n, q.shape[1], cen_a, zp, main=True), q)
 
 
 def _check_acc(layer, x, tags):
