@@ -70,6 +70,7 @@ struct G2Params {
   int64_t ldo;
   const int* row_map;   // LR1: destination row
   int col_off;          // LR1: destination column
+  int lo_off;           // LR1: > 0 -> also write the fp16 residual (v - fp16(v)) at col_off + lo_off
   float* raw_aux;       // RAW: fp32 aux plane
   int* err;
 };
@@ -323,7 +324,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
               const int acc = (int)am[j] - (p.row_zp ? zp * p.col_cs[col] : 0);
               const float v = acc == 0 ? 0.f : s_row * p.col_s[col] * (float)acc;
               if (!(fabsf(v) <= 65504.f) && p.err) atomicOr(p.err, 8 /*ERR_LR_RANGE*/);
-              o[(int64_t)orow * p.ldo + p.col_off + col] = __float2half_rn(v);
+              const __half hv = __float2half_rn(v);
+              o[(int64_t)orow * p.ldo + p.col_off + col] = hv;
+              if (p.lo_off) o[(int64_t)orow * p.ldo + p.col_off + p.lo_off + col] = __float2half_rn(v - __half2float(hv));
             }
           }
         } else {

@@ -40,7 +40,7 @@ namespace splitq {
 
 constexpr int KW_THREADS = 128;  // 4 row warps per CTA
 constexpr float KW_BAND = 4.76837158e-7f;  // 2^-21
-constexpr int KW_QCAP = 64;  // flagged-chunk queue entries per warp
+constexpr int KW_QCAP = 128;  // flagged-chunk queue entries per warp
 
 template <typename T>
 struct XW {};
@@ -119,43 +119,6 @@ struct KwConsts {
   int safe;
 };
 
-// lo / hi exact, S / zp from group_params, qspec, extra error bound in units of v.
-// The fast path has no clip: rows whose extreme codes would clip (never for
-// the reference's own S / zp up to fp64 rounding at ties) run exactly.
-__device__ __forceinline__ KwConsts kw_consts(double lo, double hi, double S, int zp,
-                                          const QSpecDev& s, double err_scale_extra) {
-  KwConsts c;
-  const double rS = __ddiv_rn(1.0, S);
-  const double vmax = fmax(fabs(lo), fabs(hi)) * rS;
-  const double err = vmax * 4.76837158203125e-07 + err_scale_extra;  // 2^-21
-  c.safe = vmax < 1048576.0;
-  int k = 10;
-  while (k < 22 && !((double)(1 << (k - 1)) > vmax + 2.0)) ++k;
-  const double ulp = ldexp(1.0, k - 23);
-  c.F = (uint32_t)(23 - k);
-  c.fm = (1u << c.F) - 1u;
-  const double Wd = floor((err + 0.5 * ulp) / ulp) + 1.0;
-  if (!(Wd < (double)(1 << (c.F - 2)))) c.safe = 0;
-  const double W = c.safe ? Wd : 1.0;
-  c.W2 = (uint32_t)(2.0 * W);
-  const int zq = s.centered ? 0 : zp;
-  const double b = 1.5 * ldexp(1.0, k) + (double)zq;
-  c.rs = (float)rS;
-  c.base = (float)b;
-  c.C = (float)(b + 0.5 + W * ulp);
-  // The fast path does not clip. Elements that would clip lie beyond
-  // qmax + 1/2 (or below qmin - 1/2) in units of code; while the row's
-  // extremes overshoot those points by at most ulp / 2, every such element
-  // is inside the flagged window (|t - tie| < W ulp + ulp / 2 rounds to
-  // <= W ulp on the t grid) and takes the exact (clipping) path. Larger
-  // overshoots (rows far from zero relative to their span) run exactly.
-  const double vl = __ddiv_rn(lo, S), vh = __ddiv_rn(hi, S);
-  const double over = vh + (double)zp - ((double)s.qmax + 0.5);
-  const double under = ((double)s.qmin - 0.5) - (vl + (double)zp);
-  if (over > 0.5 * ulp || under > 0.5 * ulp) c.safe = 0;
-  return c;
-}
-
 __device__ __forceinline__ KwConsts kw_shfl(const KwConsts& c, int src) {
   KwConsts o;
   o.rs = __shfl_sync(0xffffffffu, c.rs, src);
@@ -230,18 +193,39 @@ __device__ __forceinline__ void kw_load(const K1Params& p, const uint4* xg, int 
   d[4] = db.x; d[5] = db.y; d[6] = db.z; d[7] = db.w;
 }
 
-// z32, v32 and t bits of a chunk (bit-identical in every pass)
-__device__ __forceinline__ void kw_codes(const float (&x)[8], const float (&d)[8], const KwConsts& c,
-                                         float (&v)[8], uint32_t (&b)[8]) {
+__device__ __forceinline__ void kw_mulz(const float (&x)[8], const float (&d)[8], float (&z)[8]) {
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
-    const float2 z = kw_mul2(make_float2(x[2 * h], x[2 * h + 1]), make_float2(d[2 * h], d[2 * h + 1]));
-    const float2 vv = kw_mul2(z, make_float2(c.rs, c.rs));
+    const float2 zz = kw_mul2(make_float2(x[2 * h], x[2 * h + 1]), make_float2(d[2 * h], d[2 * h + 1]));
+    z[2 * h] = zz.x;
+    z[2 * h + 1] = zz.y;
+  }
+}
+
+// v32 and the t bits of a chunk from its z32 (bit-identical in every pass)
+__device__ __forceinline__ void kw_vt(const float (&z)[8], const KwConsts& c, float (&v)[8],
+                                      uint32_t (&b)[8]) {
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const float2 vv = kw_mul2(make_float2(z[2 * h], z[2 * h + 1]), make_float2(c.rs, c.rs));
     const float2 t = kw_add2(vv, make_float2(c.C, c.C));
     v[2 * h] = vv.x;
     v[2 * h + 1] = vv.y;
     b[2 * h] = __float_as_uint(t.x);
     b[2 * h + 1] = __float_as_uint(t.y);
+  }
+}
+
+// f = v - n for the chunk (n from the integer bits of t)
+__device__ __forceinline__ void kw_frac(const float (&v)[8], const uint32_t (&b)[8], const KwConsts& c,
+                                        float (&f)[8]) {
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const float2 nf = kw_add2(make_float2(__uint_as_float(b[2 * h] & ~c.fm), __uint_as_float(b[2 * h + 1] & ~c.fm)),
+                              make_float2(-c.base, -c.base));
+    const float2 ff = kw_add2(make_float2(v[2 * h], v[2 * h + 1]), make_float2(-nf.x, -nf.y));
+    f[2 * h] = ff.x;
+    f[2 * h + 1] = ff.y;
   }
 }
 
@@ -252,11 +236,23 @@ __device__ __forceinline__ uint32_t kw_minfrac(const uint32_t (&b)[8], uint32_t 
   return m;
 }
 
-__device__ __forceinline__ uint2 kw_pack(const uint32_t (&bytes)[8]) {
+__device__ __forceinline__ uint2 kw_pack_shift(const uint32_t (&b)[8], uint32_t F) {
+  uint32_t by[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) by[e] = b[e] >> F;
   uint2 o;
-  o.x = __byte_perm(__byte_perm(bytes[0], bytes[1], 0x0040), __byte_perm(bytes[2], bytes[3], 0x0040), 0x5410);
-  o.y = __byte_perm(__byte_perm(bytes[4], bytes[5], 0x0040), __byte_perm(bytes[6], bytes[7], 0x0040), 0x5410);
+  o.x = __byte_perm(__byte_perm(by[0], by[1], 0x0040), __byte_perm(by[2], by[3], 0x0040), 0x5410);
+  o.y = __byte_perm(__byte_perm(by[4], by[5], 0x0040), __byte_perm(by[6], by[7], 0x0040), 0x5410);
   return o;
+}
+
+__device__ __forceinline__ unsigned long long okey_d(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ounkey_d(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  return __longlong_as_double((long long)b);
 }
 
 struct KwRow {  // exact main-group parameters needed by the fallbacks
@@ -264,18 +260,23 @@ struct KwRow {  // exact main-group parameters needed by the fallbacks
   int zp;
 };
 
-// exact MAC residual e64 of channel c (layer.py:135-136, 157-159)
-__device__ __forceinline__ double kw_exact_e(const K1Params& p, float x, int c, const KwRow& r) {
-  const double z64 = __dmul_rn((double)x, __ldg(p.d_main + c));
-  const int q = kw_exact_code(z64, r.S, r.zp, p.act.qmin, p.act.qmax);
-  return __dsub_rn(z64, __dmul_rn((double)(q - r.zp), r.S));
-}
-
 template <typename T>
 __device__ __forceinline__ float kw_x(const T* xrow, int c) {
   const uint16_t h = reinterpret_cast<const uint16_t*>(xrow)[c];
-  const float2 f = XW<T>::to_f2((uint32_t)h);
-  return f.x;
+  return XW<T>::to_f2((uint32_t)h).x;
+}
+
+// exact main code of channel c: returns q, writes z64
+__device__ __forceinline__ int kw_exact_main(const K1Params& p, float x, int c, const KwRow& r,
+                                             double& z64) {
+  z64 = __dmul_rn((double)x, __ldg(p.d_main + c));
+  return kw_exact_code(z64, r.S, r.zp, p.act.qmin, p.act.qmax);
+}
+// exact MAC residual e64 of channel c (layer.py:135-136, 157-159)
+__device__ __forceinline__ double kw_exact_e(const K1Params& p, float x, int c, const KwRow& r) {
+  double z64;
+  const int q = kw_exact_main(p, x, c, r, z64);
+  return __dsub_rn(z64, __dmul_rn((double)(q - r.zp), r.S));
 }
 
 // Warp-uniform append of chunk j to the warp's flagged queue (SMEM).
@@ -289,129 +290,164 @@ __device__ __forceinline__ void kw_enqueue(uint32_t* q, int& qn, bool flag, int 
   }
 }
 
-// Pass E: main codes (+ MAC fraction extremes of the unflagged chunks).
-template <typename T, bool MAC>
-__device__ __forceinline__ void kw_pass_codes(const K1Params& p, const uint4* xg, int nchunks,
-                                              int8_t* arow, const KwConsts& c, KwExt& flo,
-                                              KwExt& fhi, uint32_t* q, int& qn) {
-  const int lane = threadIdx.x & 31;
-  for (int j0 = 0; j0 < nchunks; j0 += 32) {
-    const int j = j0 + lane;
-    bool flag = false;
-    if (j < nchunks) {
-      float x[8], d[8], v[8];
-      uint32_t b[8], bytes[8];
-      kw_load<T>(p, xg, j, x, d);
-      kw_codes(x, d, c, v, b);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) bytes[e] = b[e] >> c.F;
-      *reinterpret_cast<uint2*>(arow + 8 * j) = kw_pack(bytes);
-      flag = kw_minfrac(b, c.fm) <= c.W2;
-      if (MAC && !flag) {
-        float f[8], nf[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          f[e] = v[e] - (__uint_as_float(b[e] & ~c.fm) - c.base);
-          nf[e] = -f[e];
-        }
-        kw_ext_upd(flo, kw_min8(f), j);
-        kw_ext_upd(fhi, kw_min8(nf), j);
-      }
+// warp reductions through REDUX on order-preserving integer keys
+__device__ __forceinline__ int kw_fkey(float f) {
+  const int b = __float_as_int(f);
+  return b ^ ((b >> 31) & 0x7FFFFFFF);
+}
+__device__ __forceinline__ float kw_warp_minf(float v) {
+  const int k = __reduce_min_sync(0xffffffffu, kw_fkey(v));
+  return __int_as_float(k ^ ((k >> 31) & 0x7FFFFFFF));
+}
+// fp64 min / max of non-NaN values (+-inf allowed) in two 32-bit REDUX steps
+__device__ __forceinline__ double kw_warp_mind(double v) {
+  const unsigned long long k = okey_d(v);
+  const unsigned hi = __reduce_min_sync(0xffffffffu, (unsigned)(k >> 32));
+  const unsigned lo = __reduce_min_sync(0xffffffffu, (unsigned)(k >> 32) == hi ? (unsigned)k : 0xFFFFFFFFu);
+  return ounkey_d(((unsigned long long)hi << 32) | lo);
+}
+__device__ __forceinline__ double kw_warp_maxd(double v) {
+  const unsigned long long k = okey_d(v);
+  const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(k >> 32));
+  const unsigned lo = __reduce_max_sync(0xffffffffu, (unsigned)(k >> 32) == hi ? (unsigned)k : 0u);
+  return ounkey_d(((unsigned long long)hi << 32) | lo);
+}
+
+// compute_params (quantizer.py:118-135) returning 1 / S as well
+__device__ __forceinline__ bool kw_params(double lo, double hi, const QSpecDev& s, double* S,
+                                          int* zp, double* rS) {
+  bool ok;
+  if (s.sym) {
+    const double amax = fmax(fabs(lo), fabs(hi));
+    *S = amax > 0.0 ? __ddiv_rn(amax, (double)s.qmax) : 1.0;
+    *zp = 0;
+    ok = *S > 0.0;
+    if (!ok) *S = 1.0;
+    *rS = __ddiv_rn(1.0, *S);
+  } else {
+    double span = __dsub_rn(hi, lo);
+    if (span == 0.0) {
+      lo = fmin(lo, 0.0);
+      hi = fmax(hi, 0.0);
+      span = __dsub_rn(hi, lo);
     }
-    kw_enqueue(q, qn, flag, j);
+    *S = span > 0.0 ? __ddiv_rn(span, (double)(s.qmax - s.qmin)) : 1.0;
+    ok = *S > 0.0;
+    if (!ok) *S = 1.0;
+    *rS = __ddiv_rn(1.0, *S);
+    const double z = fmin(fmax(rha_quotient(-lo, *S, *rS), (double)s.qmin), (double)s.qmax);
+    *zp = (int)z;
+  }
+  return ok;
+}
+
+// Fast-path constants of a group from its exact parameters (see the header).
+// The fast path does not clip: elements that would clip lie beyond qmax +
+// 1/2 (or below qmin - 1/2) in code units; while the extremes overshoot those
+// points by at most ulp / 4, every such element is inside the flagged window
+// and takes the exact (clipping) path. Larger overshoots (rows far from zero
+// relative to their span) run exactly.
+__device__ __forceinline__ KwConsts kw_consts2(double lo, double hi, double S, double rS, int zp,
+                                              const QSpecDev& s, double err_extra) {
+  KwConsts c;
+  const double vl = lo * rS, vh = hi * rS;  // within 2 ulp of lo / S, hi / S
+  const double vmax = fmax(fabs(vl), fabs(vh));
+  const double err = vmax * 4.76837158203125e-07 + err_extra;  // 2^-21
+  c.safe = vmax < 1048576.0;
+  int k = 10;
+  while (k < 22 && !((double)(1 << (k - 1)) > vmax + 2.0)) ++k;
+  const double ulp = ldexp(1.0, k - 23);
+  c.F = (uint32_t)(23 - k);
+  c.fm = (1u << c.F) - 1u;
+  const double Wd = floor((err + 0.5 * ulp) / ulp) + 1.0;
+  if (!(Wd < (double)(1 << (c.F - 2)))) c.safe = 0;
+  const double W = c.safe ? Wd : 1.0;
+  c.W2 = (uint32_t)(2.0 * W);
+  const int zq = s.centered ? 0 : zp;
+  const double b = 1.5 * ldexp(1.0, k) + (double)zq;
+  c.rs = (float)rS;
+  c.base = (float)b;
+  c.C = (float)(b + 0.5 + W * ulp);
+  const double over = vh + (double)zp - ((double)s.qmax + 0.5);
+  const double under = ((double)s.qmin - 0.5) - (vl + (double)zp);
+  if (over > 0.25 * ulp || under > 0.25 * ulp) c.safe = 0;
+  return c;
+}
+
+struct KwOut {  // outlier group parameters broadcast to the warp
+  double S, rS;
+  int zp, safe;
+};
+__device__ __forceinline__ RowParams kw_rowparams(double S, double rS, int zp, int safe,
+                                                  const QSpecDev& s) {
+  RowParams r;
+  r.S = S;
+  r.rS = rS;
+  r.zp = zp;
+  r.cz = K1_MAGIC + (double)zp;
+  r.qmin = s.qmin;
+  r.qmax = s.qmax;
+  r.safe = safe != 0;
+  return r;
+}
+
+// per-lane fp64 extremes of one outlier path (channels lane, lane + 32, ...)
+template <typename T>
+__device__ __forceinline__ void kw_outlier_ext(const T* xrow, const int* cols, const double* d, int n,
+                                               double& lo, double& hi, bool& nan) {
+  const int lane = threadIdx.x & 31;
+  lo = INFINITY;
+  hi = -INFINITY;
+  for (int k = lane; k < n; k += 32) {
+    const double z = __dmul_rn((double)kw_x<T>(xrow, __ldg(cols + k)), __ldg(d + k));
+    nan |= z != z;
+    lo = fmin(lo, z);
+    hi = fmax(hi, z);
   }
 }
 
-// Pass G (text rows): MAC residual codes.
-template <typename T>
-__device__ __forceinline__ void kw_pass_mac(const K1Params& p, const uint4* xg, int nchunks,
-                                            int8_t* erow, const KwConsts& c, const KwConsts& ce,
-                                            float ratio, uint32_t* q, int& qn) {
-  const int lane = threadIdx.x & 31;
-  for (int j0 = 0; j0 < nchunks; j0 += 32) {
-    const int j = j0 + lane;
-    bool flag = false;
-    if (j < nchunks) {
-      float x[8], d[8], v[8];
-      uint32_t b[8], be[8], bytes[8];
-      kw_load<T>(p, xg, j, x, d);
-      kw_codes(x, d, c, v, b);
-#pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const float2 f = make_float2(v[2 * h] - (__uint_as_float(b[2 * h] & ~c.fm) - c.base),
-                                     v[2 * h + 1] - (__uint_as_float(b[2 * h + 1] & ~c.fm) - c.base));
-        const float2 t = kw_fma2(f, make_float2(ratio, ratio), make_float2(ce.C, ce.C));
-        be[2 * h] = __float_as_uint(t.x);
-        be[2 * h + 1] = __float_as_uint(t.y);
-      }
-#pragma unroll
-      for (int e = 0; e < 8; ++e) bytes[e] = be[e] >> ce.F;
-      *reinterpret_cast<uint2*>(erow + 8 * j) = kw_pack(bytes);
-      flag = kw_minfrac(b, c.fm) <= c.W2 || kw_minfrac(be, ce.fm) <= ce.W2;
-    }
-    kw_enqueue(q, qn, flag, j);
-  }
+// power of two rho with max(S, St, Sv) in [rho, 2 rho), and 1 / rho
+__device__ __forceinline__ void kw_rho(double m, double& rho, double& rrho) {
+  const int hi = __double2hiint(m) & 0x7FF00000;
+  rho = __hiloint2double(hi, 0);
+  rrho = __hiloint2double(0x7FE00000 - hi, 0);
 }
 
-// exact extreme over the candidate chunks of one lane (main: z; band test on z32)
-template <typename T>
-__device__ __forceinline__ double kw_rescan_z(const K1Params& p, const T* xrow, int nchunks,
-                                              const KwExt& e, float band, bool is_max) {
-  const int lane = threadIdx.x & 31;
-  double best = is_max ? -INFINITY : INFINITY;
-  const bool all = e.m2 <= band;  // a second chunk is also within the band
-  for (int j = all ? lane : e.c1; j < nchunks; j += 32) {
-    for (int u = 0; u < 8; ++u) {
-      const float x = kw_x<T>(xrow, 8 * j + u);
-      const float z = __fmul_rn(x, __ldg(p.d_main32 + 8 * j + u));
-      if ((is_max ? -z : z) <= band) {
-        const double z64 = __dmul_rn((double)x, __ldg(p.d_main + 8 * j + u));
-        best = is_max ? fmax(best, z64) : fmin(best, z64);
-      }
-    }
-    if (!all) break;
+// The z (then f) row of a warp in SMEM: two float4 planes, so lane-strided
+// 16-byte accesses are bank-conflict free.
+struct KwZ {
+  float4* a;
+  float4* b;
+  __device__ __forceinline__ void put(int j, const float (&z)[8]) const {
+    a[j] = make_float4(z[0], z[1], z[2], z[3]);
+    b[j] = make_float4(z[4], z[5], z[6], z[7]);
   }
-  return best;
-}
-
-// exact extreme of the MAC residual over a lane's candidate chunks (band test on f)
-template <typename T>
-__device__ __forceinline__ double kw_rescan_e(const K1Params& p, const T* xrow, int nchunks,
-                                              const KwExt& e, float band, bool is_max,
-                                              const KwConsts& c, const KwRow& r) {
-  const int lane = threadIdx.x & 31;
-  double best = is_max ? -INFINITY : INFINITY;
-  const bool all = e.m2 <= band;
-  for (int j = all ? lane : e.c1; j < nchunks; j += 32) {
-    for (int u = 0; u < 8; ++u) {
-      const float x = kw_x<T>(xrow, 8 * j + u);
-      const float v = __fmul_rn(__fmul_rn(x, __ldg(p.d_main32 + 8 * j + u)), c.rs);
-      const uint32_t b = __float_as_uint(__fadd_rn(v, c.C));
-      const float f = v - (__uint_as_float(b & ~c.fm) - c.base);
-      if ((is_max ? -f : f) <= band) {
-        const double e64 = kw_exact_e(p, x, 8 * j + u, r);
-        best = is_max ? fmax(best, e64) : fmin(best, e64);
-      }
-    }
-    if (!all) break;
+  __device__ __forceinline__ void get(int j, float (&z)[8]) const {
+    const float4 u = a[j], w = b[j];
+    z[0] = u.x; z[1] = u.y; z[2] = u.z; z[3] = u.w;
+    z[4] = w.x; z[5] = w.y; z[6] = w.z; z[7] = w.w;
   }
-  return best;
-}
+};
 
-template <typename T>
+template <typename T, bool SMZ>
 __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d_in) {
-  __shared__ uint32_t kw_q[KW_THREADS / 32][KW_QCAP];
-  const int lane = threadIdx.x & 31;
-  uint32_t* q = kw_q[threadIdx.x >> 5];
+  extern __shared__ __align__(16) uint8_t kw_smem[];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5, nwc = blockDim.x >> 5;
+  const int nchunks = d_in >> 3;
+  uint32_t* q = reinterpret_cast<uint32_t*>(kw_smem) + wl * KW_QCAP;
+  KwZ zs{nullptr, nullptr};
+  if (SMZ) {
+    float4* base = reinterpret_cast<float4*>(kw_smem + nwc * KW_QCAP * 4) + (size_t)wl * 2 * nchunks;
+    zs = KwZ{base, base + nchunks};
+  }
   const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nw = (int)((gridDim.x * blockDim.x) >> 5);
-  const int nchunks = d_in >> 3;
   const bool cen = p.act.centered != 0, cena = p.aux.centered != 0;
   for (int row = gw; row < p.T; row += nw) {
     const T* xrow = reinterpret_cast<const T*>(p.x) + (int64_t)row * p.ldx;
     const uint4* xg = reinterpret_cast<const uint4*>(xrow);
 
-    // ------------------------------------------------ pass A: fp32 extremes
+    // ------------------------------------------------ pass A: fp32 z and its extremes
     KwExt elo, ehi;  // ehi tracks -max
     kw_ext_init(elo);
     kw_ext_init(ehi);
@@ -432,16 +468,11 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
         nz[2 * h] = -zz.x;
         nz[2 * h + 1] = -zz.y;
       }
+      if (SMZ) zs.put(j, z);
       kw_ext_upd(elo, kw_min8(z), j);
       kw_ext_upd(ehi, kw_min8(nz), j);
     }
-    float L = elo.m1, H = ehi.m1;  // H = -max
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      L = fminf(L, __shfl_xor_sync(0xffffffffu, L, o));
-      H = fminf(H, __shfl_xor_sync(0xffffffffu, H, o));
-    }
-    // row metadata (lane 0 loads, broadcast)
+    const float L = kw_warp_minf(elo.m1), H = kw_warp_minf(ehi.m1);  // H = -max
     int slot = -1;
     if (lane == 0) {
       const uint8_t tg = p.tags ? p.tags[row] : (uint8_t)1;
@@ -449,85 +480,118 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
       slot = (p.use_mac && p.text_idx) ? p.text_idx[row] : -1;
     }
     slot = __shfl_sync(0xffffffffu, slot, 0);
-    bool bad = __any_sync(0xffffffffu, XW<T>::nonfinite(nm)) || !isfinite(L) || !isfinite(H);
 
-    // outlier paths: exact fp64 params (warp-level; quantize_fast.cuh)
-    RowParams rt, rv;
-    bool okt = true, okv = true, badt = false, badv = false;
-    rt.S = rv.S = 0.0;
-    if (p.n_text > 0) outlier_params(p, xrow, p.c_text, p.d_text, p.n_text, rt, okt, badt);
-    if (p.n_vis > 0) outlier_params(p, xrow, p.c_vis, p.d_vis, p.n_vis, rv, okv, badv);
-    if (bad || badt || badv) {
+    // outlier paths: exact fp64 extremes
+    double tlo, thi, vlo, vhi;
+    bool nan = XW<T>::nonfinite(nm);
+    kw_outlier_ext<T>(xrow, p.c_text, p.d_text, p.n_text, tlo, thi, nan);
+    kw_outlier_ext<T>(xrow, p.c_vis, p.d_vis, p.n_vis, vlo, vhi, nan);
+    if (__any_sync(0xffffffffu, nan) || !isfinite(L) || !isfinite(H)) {
+      if (lane == 0) atomicOr(p.err, ERR_NONFINITE);
+      continue;
+    }
+    tlo = kw_warp_mind(tlo);
+    thi = kw_warp_maxd(thi);
+    vlo = kw_warp_mind(vlo);
+    vhi = kw_warp_maxd(vhi);
+    if ((p.n_text > 0 && !(isfinite(tlo) && isfinite(thi))) ||
+        (p.n_vis > 0 && !(isfinite(vlo) && isfinite(vhi)))) {
       if (lane == 0) atomicOr(p.err, ERR_NONFINITE);
       continue;
     }
 
-    // ------------------------------------------------ exact main extremes
+    // ------------------------------------------------ exact main extremes: candidates
+    // are the elements within 2^-21 of the fp32 extremes (one chunk per lane, or all
+    // of the lane's chunks when its second-best chunk is also in the band)
     const float bl = L + fabsf(L) * KW_BAND + 1e-30f;
     const float bh = H + fabsf(H) * KW_BAND + 1e-30f;
     double lo64 = INFINITY, hi64 = -INFINITY;
-    if (elo.m1 <= bl) lo64 = kw_rescan_z<T>(p, xrow, nchunks, elo, bl, false);
-    if (ehi.m1 <= bh) hi64 = kw_rescan_z<T>(p, xrow, nchunks, ehi, bh, true);
-    lo64 = kw_warp_min_d(lo64);
-    hi64 = kw_warp_max_d(hi64);
-
-    // ------------------------------------------------ main group parameters (lane 0)
-    KwConsts c{};
-    double S = 1.0;
-    int zp = 0;
-    if (lane == 0) {
-      double zpd;
-      if (!group_params(lo64, hi64, p.act, &S, &zpd)) {
-        atomicOr(p.err, ERR_SCALE_ZERO);
-        S = 1.0;
+    if (elo.m1 <= bl || ehi.m1 <= bh) {
+      const bool all = elo.m2 <= bl || ehi.m2 <= bh || (elo.m1 <= bl && ehi.m1 <= bh && elo.c1 != ehi.c1);
+      for (int j = all ? lane : (elo.m1 <= bl ? elo.c1 : ehi.c1); j < nchunks; j += 32) {
+        float z[8];
+        if (SMZ) {
+          zs.get(j, z);
+        } else {
+          float x[8], d[8];
+          kw_load<T>(p, xg, j, x, d);
+          kw_mulz(x, d, z);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (z[u] <= bl || -z[u] <= bh) {
+            double z64;
+            (void)kw_exact_main;
+            z64 = __dmul_rn((double)kw_x<T>(xrow, 8 * j + u), __ldg(p.d_main + 8 * j + u));
+            if (z[u] <= bl) lo64 = fmin(lo64, z64);
+            if (-z[u] <= bh) hi64 = fmax(hi64, z64);
+          }
+        }
+        if (!all) break;
       }
-      zp = (int)zpd;
-      c = kw_consts(lo64, hi64, S, zp, p.act, 0.0);
+    }
+    lo64 = kw_warp_mind(lo64);
+    hi64 = kw_warp_maxd(hi64);
+
+    // ------------------------------------------------ group parameters, lane-parallel:
+    // lane 0 main (act spec), lane 1 text, lane 2 vision (aux spec)
+    KwConsts c{};
+    double gS = 1.0, grS = 1.0;
+    int gzp = 0, gsafe = 0;
+    {
+      const bool g_main = lane == 0, g_vis = lane == 2;
+      const double glo = g_main ? lo64 : g_vis ? vlo : tlo;
+      const double ghi = g_main ? hi64 : g_vis ? vhi : thi;
+      const QSpecDev gs = g_main ? p.act : p.aux;
+      if (lane < 3 && (lane == 0 || (lane == 1 ? p.n_text : p.n_vis) > 0)) {
+        if (!kw_params(glo, ghi, gs, &gS, &gzp, &grS)) atomicOr(p.err, ERR_SCALE_ZERO);
+        c = kw_consts2(glo, ghi, gS, grS, gzp, gs, 0.0);
+        gsafe = fmax(fabs(glo), fabs(ghi)) * grS < 536870912.0;  // 2^29 (quant_rn range)
+      }
     }
     c = kw_shfl(c, 0);
-    S = kw_shfl_d(S, 0);
-    zp = __shfl_sync(0xffffffffu, zp, 0);
-    int rexp;
-    frexp(fmax(S, fmax(rt.S, rv.S)), &rexp);
-    const double rho = ldexp(1.0, rexp - 1);
+    const double S = kw_shfl_d(gS, 0);
+    const int zp = __shfl_sync(0xffffffffu, gzp, 0);
+    const RowParams rt = kw_rowparams(kw_shfl_d(gS, 1), kw_shfl_d(grS, 1),
+                                      __shfl_sync(0xffffffffu, gzp, 1),
+                                      __shfl_sync(0xffffffffu, gsafe, 1), p.aux);
+    const RowParams rv = kw_rowparams(kw_shfl_d(gS, 2), kw_shfl_d(grS, 2),
+                                      __shfl_sync(0xffffffffu, gzp, 2),
+                                      __shfl_sync(0xffffffffu, gsafe, 2), p.aux);
+    double rho, rrho;
+    kw_rho(fmax(S, fmax(p.n_text > 0 ? rt.S : 0.0, p.n_vis > 0 ? rv.S : 0.0)), rho, rrho);
     if (lane == 0) {
       p.s_main[row] = S;
       if (p.sf_main) p.sf_main[row] = (float)S;
       p.zp_main[row] = zp;
       if (p.rho) {
         p.rho[row] = (float)rho;
-        p.lrs_main[row] = (float)(S / rho);
+        p.lrs_main[row] = (float)(S * rrho);
       }
+    } else if (lane == 1 && p.n_text > 0) {
+      p.s_text[row] = rt.S;
+      p.sf_text[row] = (float)rt.S;
+      p.zp_text[row] = rt.zp;
+    } else if (lane == 2 && p.n_vis > 0) {
+      p.s_vis[row] = rv.S;
+      p.sf_vis[row] = (float)rv.S;
+      p.zp_vis[row] = rv.zp;
     }
     const KwRow r{S, zp};
 
     // ------------------------------------------------ outlier codes + aux segments
-    if (p.n_text > 0) {
+    if (p.n_text > 0)
       outlier_codes(p, row, xrow, p.c_text, p.d_text, p.n_text, p.ld_text, p.a_text, rt,
-                    rt.S / rho, p.lr_off_t, p.kt16);
-      if (lane == 0) {
-        if (!okt) atomicOr(p.err, ERR_SCALE_ZERO);
-        p.s_text[row] = rt.S;
-        p.sf_text[row] = (float)rt.S;
-        p.zp_text[row] = rt.zp;
-      }
-    }
-    if (p.n_vis > 0) {
-      outlier_codes(p, row, xrow, p.c_vis, p.d_vis, p.n_vis, p.ld_vis, p.a_vis, rv, rv.S / rho,
+                    rt.S * rrho, p.lr_off_t, p.kt16);
+    if (p.n_vis > 0)
+      outlier_codes(p, row, xrow, p.c_vis, p.d_vis, p.n_vis, p.ld_vis, p.a_vis, rv, rv.S * rrho,
                     p.lr_off_v, p.kv16);
-      if (lane == 0) {
-        if (!okv) atomicOr(p.err, ERR_SCALE_ZERO);
-        p.s_vis[row] = rv.S;
-        p.sf_vis[row] = (float)rv.S;
-        p.zp_vis[row] = rv.zp;
-      }
-    }
     if (p.k_lr > 0) {  // the low-rank columns of the aux operand row: LR1 fills them
       uint4* lr = reinterpret_cast<uint4*>(p.lr_a + (int64_t)row * p.k_lr + p.lr_off_s);
       for (int i = lane; i < (p.k_lr - p.lr_off_s) / 8; i += 32) lr[i] = make_uint4(0, 0, 0, 0);
     }
 
-    // ------------------------------------------------ pass E: main codes
+    // ------------------------------------------------ pass E: main codes (+ f = v - n)
     int8_t* arow = p.a_main + (int64_t)row * p.ld_main;
     const bool mac = slot >= 0;
     KwExt flo, fhi;
@@ -535,27 +599,49 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     kw_ext_init(fhi);
     int qn = 0;
     if (c.safe) {
-      if (mac) kw_pass_codes<T, true>(p, xg, nchunks, arow, c, flo, fhi, q, qn);
-      else kw_pass_codes<T, false>(p, xg, nchunks, arow, c, flo, fhi, q, qn);
+      for (int j0 = 0; j0 < nchunks; j0 += 32) {
+        const int j = j0 + lane;
+        bool flag = false;
+        if (j < nchunks) {
+          float z[8], v[8];
+          uint32_t b[8];
+          if (SMZ) {
+            zs.get(j, z);
+          } else {
+            float x[8], d[8];
+            kw_load<T>(p, xg, j, x, d);
+            kw_mulz(x, d, z);
+          }
+          kw_vt(z, c, v, b);
+          *reinterpret_cast<uint2*>(arow + 8 * j) = kw_pack_shift(b, c.F);
+          flag = kw_minfrac(b, c.fm) <= c.W2;
+          if (mac) {
+            float f[8], nf[8];
+            kw_frac(v, b, c, f);
+            if (SMZ) zs.put(j, f);
+            if (!flag) {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) nf[e] = -f[e];
+              kw_ext_upd(flo, kw_min8(f), j);
+              kw_ext_upd(fhi, kw_min8(nf), j);
+            }
+          }
+        }
+        kw_enqueue(q, qn, flag, j);
+      }
     }
     // exact fallback: the flagged chunks (queue), or every chunk (unsafe row /
-    // queue overflow); elements spread over the lanes. MAC: the exact residual
+    // queue overflow), elements spread over the lanes. MAC: the exact residual
     // of every element of these chunks joins the extreme candidates.
     const bool allx = !c.safe || qn > KW_QCAP;
-#ifdef KW_DEBUG
-    if (lane == 0) {
-      atomicAdd(p.err + 1, qn);
-      if (allx) atomicAdd(p.err + 2, 1);
-    }
-#endif
+    const int qnE = allx ? 0 : qn;
     const int nfix = 8 * (allx ? nchunks : qn);
     __syncwarp();
     double xlo = INFINITY, xhi = -INFINITY;
     for (int i = lane; i < nfix; i += 32) {
       const int ch = 8 * (allx ? i >> 3 : (int)q[i >> 3]) + (i & 7);
-      const float x = kw_x<T>(xrow, ch);
-      const double z64 = __dmul_rn((double)x, __ldg(p.d_main + ch));
-      const int qc = kw_exact_code(z64, S, zp, p.act.qmin, p.act.qmax);
+      double z64;
+      const int qc = kw_exact_main(p, kw_x<T>(xrow, ch), ch, r, z64);
       arow[ch] = (int8_t)(cen ? qc - zp : qc);
       if (mac) {
         const double e64 = __dsub_rn(z64, __dmul_rn((double)(qc - zp), S));
@@ -566,57 +652,96 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     if (!mac) continue;
 
     // ------------------------------------------------ MAC: exact residual extremes
-    float FL = flo.m1, FH = fhi.m1;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      FL = fminf(FL, __shfl_xor_sync(0xffffffffu, FL, o));
-      FH = fminf(FH, __shfl_xor_sync(0xffffffffu, FH, o));
-    }
+    const float FL = kw_warp_minf(flo.m1), FH = kw_warp_minf(fhi.m1);
     // |f - e / S| <= vmax 2^-22 (+ the fp32 rounding of f): an absolute band
     const float vmaxf = fmaxf(fabsf(L), fabsf(H)) * c.rs * 1.0001f + 1.0f;
     const float fband = 2.0f * vmaxf * KW_BAND + 1e-12f;
     const float bfl = FL + fband, bfh = FH + fband;
     double elo64 = xlo, ehi64 = xhi;
-    if (!allx) {
-      if (flo.m1 <= bfl) elo64 = fmin(elo64, kw_rescan_e<T>(p, xrow, nchunks, flo, bfl, false, c, r));
-      if (fhi.m1 <= bfh) ehi64 = fmax(ehi64, kw_rescan_e<T>(p, xrow, nchunks, fhi, bfh, true, c, r));
+    if (!allx && (flo.m1 <= bfl || fhi.m1 <= bfh)) {
+      const bool all = flo.m2 <= bfl || fhi.m2 <= bfh || (flo.m1 <= bfl && fhi.m1 <= bfh && flo.c1 != fhi.c1);
+      for (int j = all ? lane : (flo.m1 <= bfl ? flo.c1 : fhi.c1); j < nchunks; j += 32) {
+        float f[8];
+        if (SMZ) {
+          zs.get(j, f);
+        } else {
+          float x[8], d[8], z[8], v[8];
+          uint32_t b[8];
+          kw_load<T>(p, xg, j, x, d);
+          kw_mulz(x, d, z);
+          kw_vt(z, c, v, b);
+          kw_frac(v, b, c, f);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (f[u] <= bfl || -f[u] <= bfh) {
+            const double e64 = kw_exact_e(p, kw_x<T>(xrow, 8 * j + u), 8 * j + u, r);
+            if (f[u] <= bfl) elo64 = fmin(elo64, e64);
+            if (-f[u] <= bfh) ehi64 = fmax(ehi64, e64);
+          }
+        }
+        if (!all) break;
+      }
     }
-    elo64 = kw_warp_min_d(elo64);
-    ehi64 = kw_warp_max_d(ehi64);
+    elo64 = kw_warp_mind(elo64);
+    ehi64 = kw_warp_maxd(ehi64);
     KwConsts ce{};
     double Se = 1.0;
     int zpe = 0;
+    float ratio = 1.f;
     if (lane == 0) {
-      double zpd;
-      if (!group_params(elo64, ehi64, p.aux, &Se, &zpd)) {
-        atomicOr(p.err, ERR_SCALE_ZERO);
-        Se = 1.0;
-      }
-      zpe = (int)zpd;
+      double rSe;
+      if (!kw_params(elo64, ehi64, p.aux, &Se, &zpe, &rSe)) atomicOr(p.err, ERR_SCALE_ZERO);
       // f carries |err| <= vmax 2^-22 in units of S: times S / Se in units of e / Se
-      ce = kw_consts(elo64, ehi64, Se, zpe, p.aux, (double)vmaxf * 2.384185791015625e-07 * (S / Se) * 1.01);
+      ce = kw_consts2(elo64, ehi64, Se, rSe, zpe, p.aux,
+                      (double)vmaxf * 2.384185791015625e-07 * (S * rSe) * 1.01);
       p.s_mac[slot] = Se;
       p.zp_mac[slot] = zpe;
-      p.lrs_mac[slot] = (float)(Se / rho);
+      p.lrs_mac[slot] = (float)(Se * rrho);
+      ratio = (float)(S * rSe);
     }
     ce = kw_shfl(ce, 0);
     Se = kw_shfl_d(Se, 0);
     zpe = __shfl_sync(0xffffffffu, zpe, 0);
-    const float ratio = (float)(S / Se);
+    ratio = __shfl_sync(0xffffffffu, ratio, 0);
 
     // ------------------------------------------------ pass G: MAC residual codes
     int8_t* erow = p.a_mac + (int64_t)slot * p.ld_main;
-    qn = 0;
+    qn = qnE;  // the chunks flagged in pass E are exact-coded here as well
     const bool allg = allx || !ce.safe;
-    __syncwarp();
-    if (!allg) kw_pass_mac<T>(p, xg, nchunks, erow, c, ce, ratio, q, qn);
-    const bool allg2 = allg || qn > KW_QCAP;
-#ifdef KW_DEBUG
-    if (lane == 0) {
-      atomicAdd(p.err + 3, qn);
-      if (allg2) atomicAdd(p.err + 2, 1 << 16);
+    if (!allg) {
+      for (int j0 = 0; j0 < nchunks; j0 += 32) {
+        const int j = j0 + lane;
+        bool flag = false;
+        if (j < nchunks) {
+          float f[8];
+          uint32_t be[8];
+          bool mflag = false;
+          if (SMZ) {
+            zs.get(j, f);
+          } else {
+            float x[8], d[8], z[8], v[8];
+            uint32_t b[8];
+            kw_load<T>(p, xg, j, x, d);
+            kw_mulz(x, d, z);
+            kw_vt(z, c, v, b);
+            kw_frac(v, b, c, f);
+            mflag = kw_minfrac(b, c.fm) <= c.W2;
+          }
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const float2 t = kw_fma2(make_float2(f[2 * h], f[2 * h + 1]), make_float2(ratio, ratio),
+                                     make_float2(ce.C, ce.C));
+            be[2 * h] = __float_as_uint(t.x);
+            be[2 * h + 1] = __float_as_uint(t.y);
+          }
+          *reinterpret_cast<uint2*>(erow + 8 * j) = kw_pack_shift(be, ce.F);
+          flag = mflag || kw_minfrac(be, ce.fm) <= ce.W2;
+        }
+        kw_enqueue(q, qn, flag, j);
+      }
     }
-#endif
+    const bool allg2 = allg || qn > KW_QCAP;
     const int ngix = 8 * (allg2 ? nchunks : qn);
     __syncwarp();
     for (int i = lane; i < ngix; i += 32) {
@@ -627,6 +752,10 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     }
     __syncwarp();
   }
+}
+
+inline size_t k1w_smem(int d_in, int warps, bool smz) {
+  return (size_t)warps * (KW_QCAP * 4 + (smz ? (size_t)d_in * 4 : 0));
 }
 
 }  // namespace splitq

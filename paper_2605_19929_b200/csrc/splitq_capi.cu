@@ -272,14 +272,16 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
   L->ld_vis = round_up(std::max<int64_t>(L->n_vis, 1), 16);
   L->r_s16 = round_up(L->r_s, 16);
   L->r_c16 = round_up(L->r_c, 16);
-  // auxiliary fp16 operand segments: [text hi|lo|hi][vision hi|lo|hi][CWS][MAC]
+  // auxiliary fp16 operand segments: [text hi|lo|hi][vision hi|lo|hi][CWS hi|lo][MAC]
+  // (the CWS first stage is split hi / lo: the branch can carry a large share
+  // of the output, so fp16 rounding of it alone would exceed the tolerance)
   L->kt16 = round_up(L->n_text, 16);
   L->kv16 = round_up(L->n_vis, 16);
   L->off_t = 0;
   L->off_v = 3 * L->kt16;
   L->off_s = L->off_v + 3 * L->kv16;
-  L->off_c = L->off_s + L->r_s16;
-  L->k_lr = (L->off_c + L->r_c16) ? round_up(L->off_c + L->r_c16, 64) : 0;
+  L->off_c = L->off_s + 2 * L->r_s;  // the fp16 MMA K step is 16 and a stage 64:
+  L->k_lr = (L->off_c + L->r_c) ? round_up(L->off_c + L->r_c, 64) : 0;  // only the total pads
 
   auto cleanup = [&](int code) {
     L->mem.release();
@@ -402,7 +404,8 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
       };
       split3(L->off_t, L->n_text, L->kt16);
       split3(L->off_v, L->n_vis, L->kv16);
-      for (int64_t c = 0; c < L->r_s; ++c) dst[L->off_s + c] = __double2half(row[L->off_s + c] / kappa);
+      for (int64_t c = 0; c < L->r_s; ++c)
+        dst[L->off_s + c] = dst[L->off_s + L->r_s + c] = __double2half(row[L->off_s + c] / kappa);
       for (int64_t c = 0; c < L->r_c; ++c) dst[L->off_c + c] = __double2half(row[L->off_c + c] / kappa);
       kap[j] = (float)(kappa * colf);
     }
@@ -570,16 +573,35 @@ int launch_k1_dt(const K1Params& k, int d_in, cudaStream_t s) {
 
 // K1 warp-per-row (fp16 / bf16 rows, d_in % 8 == 0, 16-B aligned rows):
 // fp32 fast path with certified exact fp64 fallback (k1w.cuh).
-template <typename T>
-int launch_k1w(const K1Params& k, int d_in, int device, cudaStream_t stream) {
+template <typename T, bool SMZ>
+int launch_k1w_t(const K1Params& k, int d_in, int device, cudaStream_t stream) {
+  // SMZ: one warp per CTA holding its row's z / f in SMEM; else 4 row warps per CTA
+  const int threads = SMZ ? 32 : KW_THREADS;
+  const size_t smem = k1w_smem(d_in, threads / 32, SMZ);
+  static int attr_dev[64] = {0};
+  if (device >= 0 && device < 64 && !attr_dev[device]) {
+    CUDA_TRY(cudaFuncSetAttribute(k1w_kernel<T, SMZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  200 * 1024));
+    attr_dev[device] = 1;
+  }
   int per_sm = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1w_kernel<T>, KW_THREADS, 0));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1w_kernel<T, SMZ>, threads, smem));
   if (per_sm < 1) return SPLITQ_ERR_UNSUPPORTED;
-  const int64_t warps = (int64_t)per_sm * sm_count(device) * (KW_THREADS / 32);
-  const int64_t grid = (std::min<int64_t>(k.T, warps) + KW_THREADS / 32 - 1) / (KW_THREADS / 32);
-  k1w_kernel<T><<<(unsigned)grid, KW_THREADS, 0, stream>>>(k, d_in);
+  const int64_t warps = (int64_t)per_sm * sm_count(device) * (threads / 32);
+  const int64_t grid = (std::min<int64_t>(k.T, warps) + threads / 32 - 1) / (threads / 32);
+  k1w_kernel<T, SMZ><<<(unsigned)grid, threads, smem, stream>>>(k, d_in);
   CUDA_TRY(cudaGetLastError());
   return SPLITQ_OK;
+}
+
+template <typename T>
+int launch_k1w(const K1Params& k, int d_in, int device, cudaStream_t stream) {
+  static const char* env = getenv("SPLITQ_K1_SMZ");
+  // SMEM-staged z / f saves the recompute but caps residency at ~15 warps /
+  // SM; the recompute variant measured faster (0.80 vs 1.00 ms, 7B q-proj)
+  const bool smz = env ? env[0] == '1' : false;
+  return smz ? launch_k1w_t<T, true>(k, d_in, device, stream)
+             : launch_k1w_t<T, false>(k, d_in, device, stream);
 }
 
 bool k1v3_eligible(const K1Params& k, int d_in) {
@@ -718,7 +740,7 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   // ---- low-rank first stages: fp16 columns of the auxiliary operand
   auto lr1 = [&](const void* a_codes, bool a_signed, const int8_t* bu, const float* su,
                  const int* csu, int64_t r, const float* row_s, const int* row_zp,
-                 const int* m_count, const int* row_map, int64_t col_off) -> int {
+                 const int* m_count, const int* row_map, int64_t col_off, int64_t lo_off) -> int {
     GemmLaunch g{};
     g.p.M = (int)T;
     g.p.m_count = m_count;
@@ -734,6 +756,7 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
     g.p.out = lr_a;
     g.p.ldo = L->k_lr;
     g.p.col_off = (int)col_off;
+    g.p.lo_off = (int)lo_off;
     g.p.row_map = row_map;
     g.p.err = err;
     bool ok = map_i8(&g.maps.a, a_codes, T, L->k_nat, L->ld_main, 128) &&
@@ -745,12 +768,12 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   if (L->r_s &&
       (rc = lr1(at(W.a_main), L->act.centered, L->b_us, L->s_us, L->cs_us, L->r_s,
                 (const float*)at(W.lrs_main), L->act.centered ? nullptr : (const int*)at(W.zp_main),
-                nullptr, nullptr, L->off_s)))
+                nullptr, nullptr, L->off_s, L->r_s)))
     return rc;
   if (L->r_c &&
       (rc = lr1(at(W.a_mac), L->aux.centered, L->b_uc, L->s_uc, L->cs_uc, L->r_c,
                 (const float*)at(W.lrs_mac), L->aux.centered ? nullptr : (const int*)at(W.zp_mac),
-                n_text, text_rows, L->off_c)))
+                n_text, text_rows, L->off_c, 0)))
     return rc;
   if (prof && (rc = prof_record(L, stream))) return rc;
 

@@ -8,6 +8,8 @@ check), non-finite values and bad tags. Every case checks codes, scales and
 zero points bit-exactly and the fp32 output within 1e-3 of the output RMS.
 """
 
+import zlib
+
 import numpy as np
 import pytest
 
@@ -118,7 +120,7 @@ SHAPES = {
 @pytest.mark.parametrize("name", sorted(SHAPES))
 def test_half_input_parity(name, dt):
     sh = dict(SHAPES[name])
-    rng = np.random.default_rng(hash(name) % 2**31)
+    rng = np.random.default_rng(zlib.crc32(name.encode()) + (7 if dt is torch.bfloat16 else 0))
     T, d_in = sh["T"], sh["d_in"]
     tags = wl.tags_with_spans(rng, T, T // 4)
     x = rng.standard_normal((T, d_in))
