@@ -477,7 +477,14 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     if (lane == 0) {
       const uint8_t tg = p.tags ? p.tags[row] : (uint8_t)1;
       if (tg > 1) atomicOr(p.err, ERR_BAD_TAG);
-      slot = (p.use_mac && p.text_idx) ? p.text_idx[row] : -1;
+      if (p.use_mac && tg == 0) {
+        if (p.mac_count) {
+          slot = atomicAdd(p.mac_count, 1);
+          p.mac_rows[slot] = row;
+        } else if (p.text_idx) {
+          slot = p.text_idx[row];
+        }
+      }
     }
     slot = __shfl_sync(0xffffffffu, slot, 0);
 

@@ -191,6 +191,8 @@ struct K1Params {
   // MAC residual (compact text rows)
   int use_mac;
   const int* text_idx;
+  int* mac_count;  // K1w: MAC slots are claimed with an atomic (order-free; rows independent)
+  int* mac_rows;   //      mac_rows[slot] = row
   int8_t* a_mac;
   double* s_mac;
   int* zp_mac;

@@ -680,8 +680,6 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   const bool prof = (flags & SPLITQ_FWD_PROFILE) != 0;
   if (prof && (rc = prof_record(L, stream))) return rc;
   CUDA_TRY(cudaMemsetAsync(err, 0, 16, stream));
-  compact_text_rows_kernel<<<1, 1024, 0, stream>>>(tags, (int)T, text_idx, text_rows, n_text, err);
-  CUDA_TRY(cudaGetLastError());
 
   K1Params k{};
   k.x = x;
@@ -732,6 +730,16 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   k.kt16 = (int)L->kt16;
   k.kv16 = (int)L->kv16;
   k.err = err;
+  if (k1v3_eligible(k, (int)L->d_in) && !getenv("SPLITQ_K1_LEGACY")) {
+    // K1w claims the compact MAC rows itself (text_rows[slot] = row, order-free)
+    CUDA_TRY(cudaMemsetAsync(n_text, 0, sizeof(int), stream));
+    k.mac_count = n_text;
+    k.mac_rows = text_rows;
+    k.text_idx = nullptr;
+  } else {
+    compact_text_rows_kernel<<<1, 1024, 0, stream>>>(tags, (int)T, text_idx, text_rows, n_text, err);
+    CUDA_TRY(cudaGetLastError());
+  }
   if ((rc = launch_k1(k, (int)L->d_in, L->device, stream))) return rc;
   if (prof && (rc = prof_record(L, stream))) return rc;
 

@@ -90,11 +90,16 @@ def _check_codes(layer, x, tags):
         q, s, z = act["mac"]
         n = q.shape[0]
         assert int(_ws_view(ws, lay.n_text, np.int32, 1)[0]) == n
-        np.testing.assert_array_equal(_ws_view(ws, lay.text_rows, np.int32, n), act["text_rows"])
-        zp = _ws_view(ws, lay.zp_mac, np.int32, n).astype(np.int64)
+        # compact MAC rows may be claimed in any order: slot -> row map
+        rows = _ws_view(ws, lay.text_rows, np.int32, n)
+        np.testing.assert_array_equal(np.sort(rows), act["text_rows"])
+        order = np.argsort(rows, kind="stable")
+        zp = _ws_view(ws, lay.zp_mac, np.int32, n).astype(np.int64)[order]
         np.testing.assert_array_equal(zp, z)
-        np.testing.assert_array_equal(_ws_view(ws, lay.s_mac, np.float64, n), s)
-        np.testing.assert_array_equal(codes_of(lay.a_mac, lay.ld_main, n, q.shape[1], cen_a, zp, main=True), q)
+        np.testing.assert_array_equal(_ws_view(ws, lay.s_mac, np.float64, n)[order], s)
+        codes = codes_of(lay.a_mac, lay.ld_main, n, q.shape[1], cen_a,
+                         _ws_view(ws, lay.zp_mac, np.int32, n).astype(np.int64), main=True)
+        np.testing.assert_array_equal(codes[order], q)
 
 
 def _check_acc(layer, x, tags):

@@ -88,11 +88,14 @@ def _check(layer, xd, x64, tags):
         q, s, z = act["mac"]
         n = q.shape[0]
         assert int(view(lay.n_text, np.int32, 1)[0]) == n
+        rows = view(lay.text_rows, np.int32, n)  # slot -> row (claimed in any order)
+        np.testing.assert_array_equal(np.sort(rows), act["text_rows"])
+        order = np.argsort(rows, kind="stable")
         zp = view(lay.zp_mac, np.int32, n).astype(np.int64)
-        np.testing.assert_array_equal(zp, z)
-        np.testing.assert_array_equal(view(lay.s_mac, np.float64, n), s)
+        np.testing.assert_array_equal(zp[order], z)
+        np.testing.assert_array_equal(view(lay.s_mac, np.float64, n)[order], s)
         np.testing.assert_array_equal(codes_of(lay.a_mac, lay.ld_main, n, q.shape[1],
-                                               lay.code_centered_aux, zp, True), q)
+                                               lay.code_centered_aux, zp, True)[order], q)
     ref = orc.forward(L, x64, tags)
     rms = np.sqrt(np.mean(ref ** 2))
     err = np.max(np.abs(y - ref)) / rms
