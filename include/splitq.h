@@ -61,6 +61,8 @@ extern "C" {
 /* forward flags */
 #define SPLITQ_FWD_RAW 1     /* y receives raw accumulators (see splitq_forward) */
 #define SPLITQ_FWD_PROFILE 2 /* record stage events on the stream (splitq_profile_read) */
+#define SPLITQ_FWD_UNPACKED 4 /* main GEMM streams the int8 weight copy instead of the packed
+                                 4-bit codes (W <= 4 bits); for A/B parity checks */
 
 typedef struct splitq_layer_s* splitq_layer_t;
 

@@ -15,7 +15,7 @@ CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_NAME = "libsplitq_b200.so"
 LIB_PATH = os.path.join(PKG_DIR, LIB_NAME)
 SOURCES = ["splitq_capi.cu", "mocd.cu"]
-HEADERS = ["gemm_sm100.cuh", "quantize.cuh", "quantize_fast.cuh", "sm100_ptx.cuh", "tma_host.cuh", "mocd.cuh", "k1w.cuh"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -22,6 +22,7 @@ SPLITQ_ERR_NCCL = -5
 F16, F32, F64, BF16 = 0, 1, 2, 3
 FWD_RAW = 1
 FWD_PROFILE = 2
+FWD_UNPACKED = 4
 
 STATUS_NONFINITE = 1
 STATUS_SCALE = 2

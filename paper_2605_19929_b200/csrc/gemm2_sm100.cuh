@@ -13,9 +13,20 @@
 //     B_aux (fp16, per column) = [text hi | hi | lo][vision hi | hi | lo][CWS v][MAC v]
 //   (the hi/lo splits make the outlier products exact to ~2^-22)
 //   y = S_a[i] S_w[j] (R_main - zp_i cs_j) + rho_i kappa_j R_aux
-// Warp roles per CTA (192 threads): 0 TMA producer, 1 TMEM alloc + MMA issue
-// (leader CTA only), 2..5 epilogue. Accumulators are double-buffered so the
-// epilogue of tile t overlaps the MMAs of tile t+1.
+// Warp roles per CTA (320 threads): 0 TMA producer, 1 TMEM alloc + MMA issue
+// (leader CTA only), 2..5 epilogue, 6..9 weight unpack. Accumulators are
+// double-buffered so the epilogue of tile t overlaps the MMAs of tile t+1.
+//
+// Packed weights (p.packed_b): the main B operand lives in HBM as 4-bit
+// two's-complement codes (W4, and W3 in the same container), two per byte,
+// interleaved so that byte i of each 32-bit word holds codes 8g+i (low nibble)
+// and 8g+4+i (high nibble). Each CTA's producer TMA-loads the packed half-box
+// [bn/2 rows x 64 B] into a staging buffer (local mbarrier bfull); the unpack
+// warps sign-extend it to s8 and store it in the 128-byte-swizzled K-major
+// layout the UMMA descriptor expects (16-B chunk c of row r at c ^ (r & 7)),
+// fence the generic-proxy writes for the async proxy, and arrive on the
+// leader CTA's full barrier, which therefore counts the A bytes (TMA) plus one
+// arrival per CTA's unpack group.
 #pragma once
 #include <cstdint>
 #include <cuda.h>
@@ -32,14 +43,19 @@ constexpr int G2_BN_MAX = 256;             // max tile N without it
 constexpr int G2_A_BYTES = 128 * 128;      // per CTA: 128 rows x 128 B
 constexpr int G2_MAX_STAGES = 12;
 constexpr int G2_RING_BYTES = 192 * 1024;  // SMEM ring: stages of A (16 KB) + B (bn * 64 B)
-constexpr int G2_THREADS = 192;
+constexpr int G2_THREADS = 192;         // producer, MMA, 4 epilogue warps
+constexpr int G2_THREADS_PACKED = 320;  // + 4 weight-unpack warps
+constexpr int G2_CONV_WARP0 = 6;  // warps 6..9 unpack packed weights
 constexpr int G2_TMEM_COLS = 512;
 constexpr int G2_SMEM_BYTES = G2_RING_BYTES + 1024 + 512;
 
-// stage geometry for a tile width: per CTA an A box (128 x 128 B) and a B box (bn/2 x 128 B)
-__host__ __device__ inline int g2_stage_bytes(int bn) { return G2_A_BYTES + bn * 64; }
-__host__ __device__ inline int g2_stages(int bn) {
-  const int s = G2_RING_BYTES / g2_stage_bytes(bn);
+// stage geometry for a tile width: per CTA an A box (128 x 128 B), a B box
+// (bn/2 x 128 B) and, with packed weights, the packed staging box (bn/2 x 64 B)
+__host__ __device__ inline int g2_stage_bytes(int bn, int packed) {
+  return G2_A_BYTES + bn * 64 + (packed ? bn * 32 : 0);
+}
+__host__ __device__ inline int g2_stages(int bn, int packed) {
+  const int s = G2_RING_BYTES / g2_stage_bytes(bn, packed);
   return s < G2_MAX_STAGES ? s : G2_MAX_STAGES;
 }
 
@@ -47,7 +63,7 @@ enum G2Mode : int { G2_SPLIT = 0, G2_RAW = 1, G2_LR1 = 2 };
 enum G2Out : int { G2_F32 = 0, G2_F16 = 1, G2_BF16 = 2 };
 
 struct G2Maps {
-  CUtensorMap a, b;      // main int8 operands: A [rows x K], B [N x K]
+  CUtensorMap a, b;      // main int8 operands: A [rows x K], B [N x K] (b: packed [N x K/2] when packed_b)
   CUtensorMap xa, xb;    // aux fp16 operands: A_aux [rows x K_aux], B_aux [N x K_aux]
 };
 
@@ -60,6 +76,7 @@ struct G2Params {
   int k_aux;          // fp16 K (multiple of 64; 0 = no aux branch)
   uint32_t idesc_main, idesc_aux;
   int mode, out_dtype;
+  int packed_b;         // main B operand as packed 4-bit codes (see header)
   const float* row_s;   // S_a (SPLIT) or S/rho (LR1)
   const int* row_zp;    // zero points when A codes are u8
   const float* row_rho;
@@ -90,6 +107,12 @@ __device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
   uint32_t out;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_u32(p)), "r"(rank));
   return out;
+}
+// arrive on a (possibly remote) cluster barrier with the default .release.cta
+// semantics: no GPU-scope membar (the unpack warps' generic-proxy writes are
+// ordered for the tensor core by fence.proxy.async before this arrive)
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
@@ -152,16 +175,19 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
+template <bool PACKED>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_PACKED : G2_THREADS, 1)
     splitq_gemm2_kernel(const __grid_constant__ G2Maps maps, const G2Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  const int STAGES = g2_stages(p.bn);
-  const int STAGE_BYTES = g2_stage_bytes(p.bn);
+  const int STAGES = g2_stages(p.bn, PACKED);
+  const int STAGE_BYTES = g2_stage_bytes(p.bn, PACKED);
+  const int B_BYTES = p.bn * 64;  // per CTA: bn/2 rows x 128 B
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + G2_RING_BYTES);
   uint64_t* empty = full + G2_MAX_STAGES;
-  uint64_t* tfull = empty + G2_MAX_STAGES;  // [2]
+  uint64_t* bfull = empty + G2_MAX_STAGES;  // packed staging landed (local)
+  uint64_t* tfull = bfull + G2_MAX_STAGES;  // [2]
   uint64_t* tempty = tfull + 2;          // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -178,8 +204,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], PACKED ? 3 : 1);  // producer (A tx) [+ one unpack arrival per CTA]
       mbar_init(&empty[s], 1);
+      mbar_init(&bfull[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -203,6 +230,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t tx = 2u * (G2_A_BYTES + (uint32_t)(p.bn / 2) * 128u);
+      const uint32_t tx_a = 2u * G2_A_BYTES;               // packed main stages: A only
+      const uint32_t tx_bp = (uint32_t)(p.bn / 2) * 64u;   // local packed staging box
       for (int tile = pair; tile < num_tiles; tile += num_pairs) {
         const int m0 = (tile / n_tiles) * G2_BM + (int)rank * 128;
         const int n0 = (tile % n_tiles) * p.bn + (int)rank * (p.bn / 2);
@@ -211,14 +240,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + G2_A_BYTES;
           if (elect_one()) {
-            if (leader) mbar_arrive_expect_tx(&full[stage], tx);
+            const bool pk = PACKED && v >= n_aux;
+            if (leader) mbar_arrive_expect_tx(&full[stage], pk ? tx_a : tx);
+            // bfull advances once per ring slot use (packed: with the staging
+            // bytes; otherwise a plain arrival) so its phase stays in lockstep
+            // with the ring phase the unpack warps wait on
             if (v < n_aux) {
               tma_load_2d_pair(sa, &maps.xa, &full[stage], v * 64, m0);
               tma_load_2d_pair(sb, &maps.xb, &full[stage], v * 64, n0);
+              if (PACKED) mbar_arrive(&bfull[stage]);
             } else {
               const int c = v - n_aux;
               tma_load_2d_pair(sa, &maps.a, &full[stage], c * 128, m0);
-              tma_load_2d_pair(sb, &maps.b, &full[stage], c * 128, n0);
+              if (pk) {
+                mbar_arrive_expect_tx(&bfull[stage], tx_bp);
+                tma_load_2d(sb + B_BYTES, &maps.b, &bfull[stage], c * 64, n0);
+              } else {
+                tma_load_2d_pair(sb, &maps.b, &full[stage], c * 128, n0);
+                if (PACKED) mbar_arrive(&bfull[stage]);
+              }
             }
           }
           __syncwarp();
@@ -271,6 +311,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
         }
         if (elect_one()) tc_commit_pair(&tfull[b]);
         __syncwarp();
+      }
+    }
+  } else if (PACKED && warp >= G2_CONV_WARP0) {
+    // ================================================== weight unpack (warps 6..9, both CTAs)
+    // Ring slots are dealt round-robin to the four unpack warps, so up to four
+    // slots are being unpacked at once; each warp unpacks a whole slot
+    // (bn/2 rows x 8 16-byte chunks) and its lane 0 arrives on the leader's
+    // full barrier for that slot (one arrival per CTA).
+    const int cw = warp - G2_CONV_WARP0;
+    const uint32_t full_leader = mapa_shared(&full[0], 0);
+    const int outs = (p.bn / 2) * 8;  // 16-byte output chunks per slot
+    if (num_tiles > 0) {
+      int stage = 0, seq = 0;
+      uint32_t phase = 0;
+      for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+        for (int v = 0; v < stages_per_tile; ++v, ++seq) {
+          if ((seq & 3) == cw) {
+            mbar_wait(&empty[stage], phase ^ 1);  // previous use of the slot drained
+            if (v >= n_aux) {
+              mbar_wait(&bfull[stage], phase);
+              uint8_t* sb = smem + stage * STAGE_BYTES + G2_A_BYTES;
+              const uint8_t* sp = sb + B_BYTES;
+#pragma unroll 4
+              for (int o = lane; o < outs; o += 32) {
+                const int r = o >> 3, c = o & 7;
+                const uint2 w = *reinterpret_cast<const uint2*>(sp + r * 64 + c * 8);
+                const uint32_t w0h = w.x >> 4, w1h = w.y >> 4;
+                uint4 out;  // sign-extend 4-bit codes: (v & 0x0F..) | ((v & 0x08..) * 0x1E)
+                out.x = (w.x & 0x0F0F0F0Fu) | ((w.x & 0x08080808u) * 0x1Eu);
+                out.y = (w0h & 0x0F0F0F0Fu) | ((w0h & 0x08080808u) * 0x1Eu);
+                out.z = (w.y & 0x0F0F0F0Fu) | ((w.y & 0x08080808u) * 0x1Eu);
+                out.w = (w1h & 0x0F0F0F0Fu) | ((w1h & 0x08080808u) * 0x1Eu);
+                *reinterpret_cast<uint4*>(sb + r * 128 + ((c ^ (r & 7)) << 4)) = out;
+              }
+              fence_proxy_async();  // generic-proxy SMEM writes -> async proxy (UMMA)
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(full_leader + (uint32_t)(stage * sizeof(uint64_t)));
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
       }
     }
   } else {

@@ -155,6 +155,7 @@ struct splitq_layer_s {
   int* c_text = nullptr; double* d_text = nullptr;
   int* c_vis = nullptr; double* d_vis = nullptr;
   int8_t* b_main = nullptr; float* s_main = nullptr; int* cs_main = nullptr;
+  uint8_t* bp_main = nullptr;  // packed 4-bit main weights [d_out x ld_main / 2] (W <= 4 bits)
   int8_t* b_us = nullptr; float* s_us = nullptr; int* cs_us = nullptr;
   int8_t* b_uc = nullptr; float* s_uc = nullptr; int* cs_uc = nullptr;
   __half* b_lr = nullptr; float* kappa = nullptr;
@@ -320,6 +321,24 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
   if ((rc = pack_weight(L, d->q_main, d->s_main, d->n_main, N, L->ld_main, &L->b_main, &L->s_main,
                         &L->cs_main, 1.0, nullptr, d->c_main)))
     return cleanup(rc);
+  if (wsp.qmax - wsp.qmin <= 15 && !getenv("SPLITQ_UNPACKED_W")) {
+    // W <= 4 bits: the main GEMM streams 4-bit codes (two per byte; byte i of
+    // each 32-bit word holds codes 8g+i and 8g+4+i), unpacked in SMEM
+    std::vector<uint8_t> bp((size_t)N * (L->ld_main / 2), 0);
+    std::vector<int8_t> full((size_t)N * L->ld_main, 0);
+    for (int64_t k = 0; k < d->n_main; ++k) {
+      const int64_t kk = d->c_main[k];
+      for (int64_t n = 0; n < N; ++n) full[(size_t)n * L->ld_main + kk] = d->q_main[k * N + n];
+    }
+    for (int64_t n = 0; n < N; ++n) {
+      const int8_t* src = full.data() + (size_t)n * L->ld_main;
+      uint8_t* dst = bp.data() + (size_t)n * (L->ld_main / 2);
+      for (int64_t g = 0; g < L->ld_main / 8; ++g)
+        for (int i = 0; i < 4; ++i)
+          dst[4 * g + i] = (uint8_t)((src[8 * g + i] & 0xF) | ((src[8 * g + 4 + i] & 0xF) << 4));
+    }
+    if ((rc = L->mem.upload(&L->bp_main, bp.data(), bp.size()))) return cleanup(rc);
+  }
   if (L->k_lr) {
     // Low-rank first stage: A_lr[i, c] = (S_a[i] / rho_i) * (S_u[c] / sigma_c) * acc[i, c]
     // with sigma_c a power of two bounding |A_lr| by 2^15 (fp16-safe for any input).
@@ -487,18 +506,25 @@ struct GemmLaunch {
 };
 
 // Persistent launch: one CTA pair per two SMs (cluster of 2).
+inline bool raw_unpacked(int flags) { return (flags & SPLITQ_FWD_UNPACKED) != 0; }
+
 int launch_gemm(GemmLaunch& g, int device, int64_t max_rows, cudaStream_t stream) {
-  if (device >= 0 && device < 64 && !g_gemm_attr_set[device]) {
-    CUDA_TRY(cudaFuncSetAttribute(splitq_gemm2_kernel,
+  static bool attr[64][2] = {};
+  const int pk = g.p.packed_b ? 1 : 0;
+  if (device >= 0 && device < 64 && !attr[device][pk]) {
+    CUDA_TRY(cudaFuncSetAttribute(pk ? splitq_gemm2_kernel<true> : splitq_gemm2_kernel<false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, G2_SMEM_BYTES));
-    g_gemm_attr_set[device] = true;
+    attr[device][pk] = true;
   }
   const int64_t m_tiles = (max_rows + G2_BM - 1) / G2_BM;
   const int64_t n_tiles = (g.p.N + g.p.bn - 1) / g.p.bn;
   const int64_t tiles = m_tiles * n_tiles;
   if (tiles == 0) return SPLITQ_OK;
   const int pairs = (int)std::min<int64_t>(tiles, sm_count(device) / 2);
-  splitq_gemm2_kernel<<<2 * pairs, G2_THREADS, G2_SMEM_BYTES, stream>>>(g.maps, g.p);
+  if (pk)
+    splitq_gemm2_kernel<true><<<2 * pairs, G2_THREADS_PACKED, G2_SMEM_BYTES, stream>>>(g.maps, g.p);
+  else
+    splitq_gemm2_kernel<false><<<2 * pairs, G2_THREADS, G2_SMEM_BYTES, stream>>>(g.maps, g.p);
   CUDA_TRY(cudaGetLastError());
   return SPLITQ_OK;
 }
@@ -805,8 +831,21 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   g.p.out = y;
   g.p.ldo = y_ld;
   if (raw) g.p.raw_aux = reinterpret_cast<float*>(reinterpret_cast<int*>(y) + T * y_ld);
-  bool ok = map_i8(&g.maps.a, at(W.a_main), T, L->k_nat, L->ld_main, 128) &&
-            map_i8(&g.maps.b, L->b_main, L->d_out, L->k_nat, L->ld_main, g.p.bn / 2);
+  bool ok = map_i8(&g.maps.a, at(W.a_main), T, L->k_nat, L->ld_main, 128);
+  // Packed 4-bit weights pay where the GEMM streams weights (few token rows:
+  // decode); for large token counts the kernel is tensor / SMEM-bandwidth
+  // bound and the SMEM unpack traffic (+50% over the UMMA operand reads at
+  // 256 x 128 tiles) costs more than it saves, so the int8 expansion is used.
+  static const long packed_max_rows = getenv("SPLITQ_PACKED_MAX_ROWS")
+                                          ? atol(getenv("SPLITQ_PACKED_MAX_ROWS")) : 2048;
+  if (L->bp_main && !raw_unpacked(flags) && T <= packed_max_rows) {
+    g.p.packed_b = 1;
+    ok = ok && make_map_2d(&g.maps.b, L->bp_main, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, L->d_out,
+                           L->ld_main / 2, L->ld_main / 2, g.p.bn / 2, 64,
+                           CU_TENSOR_MAP_SWIZZLE_NONE);
+  } else {
+    ok = ok && map_i8(&g.maps.b, L->b_main, L->d_out, L->k_nat, L->ld_main, g.p.bn / 2);
+  }
   g.maps.xa = g.maps.xb = g.maps.a;
   if (ok && L->k_lr)
     ok = map_f16(&g.maps.xa, lr_a, T, L->k_lr, L->k_lr, 128) &&

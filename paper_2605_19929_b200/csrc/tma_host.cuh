@@ -35,7 +35,8 @@ inline EncodeTiledFn get_encode_fn() {
 // paths (the map is then never dereferenced by any stage).
 inline bool make_map_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int elem_bytes,
                         uint64_t rows, uint64_t cols, uint64_t row_stride_bytes, uint32_t box_rows,
-                        uint32_t box_cols) {
+                        uint32_t box_cols,
+                        CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
   std::memset(map, 0, sizeof(*map));
   EncodeTiledFn enc = get_encode_fn();
   if (!enc || base == nullptr) return false;
@@ -47,7 +48,7 @@ inline bool make_map_2d(CUtensorMap* map, const void* base, CUtensorMapDataType 
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }

@@ -150,7 +150,7 @@ class GpuLayer:
         return ws
 
     def run(self, x, tags, y=None, out_dtype=None, raw=False, check=True, ws=None,
-            profile=False):
+            profile=False, unpacked=False):
         """Launch the forward on the current stream. x: CUDA [T x >=d_in]
         (f16/bf16/f32/f64, unit column stride), tags: CUDA uint8 [T]."""
         torch = _torch()
@@ -175,7 +175,8 @@ class GpuLayer:
         _lib.check(lib.splitq_forward(self.handle, _ptr(x), _dtype_code(x.dtype), x.stride(0),
                                       _ptr(tags), T, _ptr(y), ydt, y_ld, _ptr(ws),
                                       ws.numel(), _stream(),
-                                      (_lib.FWD_RAW if raw else 0) | (_lib.FWD_PROFILE if profile else 0)))
+                                      (_lib.FWD_RAW if raw else 0) | (_lib.FWD_PROFILE if profile else 0)
+                                      | (_lib.FWD_UNPACKED if unpacked else 0)))
         if check:
             st = C.c_int32()
             _lib.check(lib.splitq_read_status(_ptr(ws), _stream(), C.byref(st)))

@@ -273,3 +273,18 @@ def test_quantize_rows_matches_oracle():
         np.testing.assert_array_equal(q, qo)
         np.testing.assert_array_equal(p.scales, so)
         np.testing.assert_array_equal(p.zero_points, zo)
+
+
+@pytest.mark.parametrize("name", ["c1_small", "a3w3", "a8w4", "k110_down"])
+def test_packed_weights_match_int8_weights(name):
+    """The main GEMM streams 4-bit packed weight codes (unpacked in SMEM);
+    its raw int32 accumulators and outputs equal those of the int8 copy."""
+    from paper_2605_19929_b200 import runtime
+    layer, x, tags = _case(**CASES[name])
+    g = runtime.packed(layer)
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    td = torch.from_numpy(tags).cuda()
+    for raw in (True, False):
+        a = g.run(xd, td, raw=raw).cpu().numpy()
+        b = g.run(xd, td, raw=raw, unpacked=True).cpu().numpy()
+        np.testing.assert_array_equal(a, b)
