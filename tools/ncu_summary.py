@@ -68,13 +68,15 @@ def full(path, out):
         if m in WANT:
             key = f'{row[h.index("ID")]}:{row[h.index("Kernel Name")].split("(")[0]}'
             kernels[key][m] = f'{row[h.index("Metric Value")]} {row[h.index("Metric Unit")]}'.strip()
-    r = list(csv.reader(io.StringIO(raw)))
+    r = list(csv.reader(io.StringIO(raw))) or [[]]
     h = r[0]
-    for row in r[2:]:
+    for row in (r[2:] if "ID" in h else []):
         key = f'{row[h.index("ID")]}:{row[h.index("Kernel Name")].split("(")[0]}'
-        for name in RAW:
-            if name in h:
-                kernels[key][name] = row[h.index(name)]
+        for i, name in enumerate(h):
+            base = name.split(".", 1)[1] if name.startswith("TPC.") else name
+            if base in RAW or any(t in name for t in ("pipe_tensor", "mem_tensor_cycles")):
+                if name.endswith(("pct_of_peak_sustained_elapsed", "pct_of_peak_sustained_active", ".sum")):
+                    kernels[key][name] = row[i]
         stalls = {}
         for i, name in enumerate(h):
             if name.startswith("smsp__average_warps_issue_stalled") and name.endswith("per_issue_active.ratio"):
