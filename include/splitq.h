@@ -121,6 +121,7 @@ typedef struct {
   int32_t code_centered_aux;
   int32_t main_natural;                            /* 1: main / MAC codes in natural channel order */
   int32_t reserved;
+  int64_t acc_scratch, acc_scratch_bytes;          /* split-K partial accumulators (decode-sized calls) */
 } splitq_ws_layout_t;
 
 const char* splitq_last_error(void);

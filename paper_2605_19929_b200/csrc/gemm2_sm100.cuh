@@ -59,7 +59,13 @@ __host__ __device__ inline int g2_stages(int bn, int packed) {
   return s < G2_MAX_STAGES ? s : G2_MAX_STAGES;
 }
 
-enum G2Mode : int { G2_SPLIT = 0, G2_RAW = 1, G2_LR1 = 2 };
+enum G2Mode : int { G2_SPLIT = 0, G2_RAW = 1, G2_LR1 = 2, G2_ACC = 3 };
+// G2_ACC (split-K): work item = (tile, K range); the epilogue adds the int32
+// main / fp32 aux partial accumulators into acc_i32 / acc_f32 [rows x ld_acc]
+// with RED atomics, and g2_finalize_* apply the SPLIT / LR1 / RAW epilogue
+// (same arithmetic, g2_epi_*) once every range has landed. The int32 sum is
+// exact in any order; the fp32 auxiliary sum is order-dependent in its last
+// bits only.
 enum G2Out : int { G2_F32 = 0, G2_F16 = 1, G2_BF16 = 2 };
 
 struct G2Maps {
@@ -90,7 +96,37 @@ struct G2Params {
   int lo_off;           // LR1: > 0 -> also write the fp16 residual (v - fp16(v)) at col_off + lo_off
   float* raw_aux;       // RAW: fp32 aux plane
   int* err;
+  int k_split;          // >= 1: K ranges per tile (G2_ACC when > 1)
+  int* acc_i32;         // G2_ACC scratch (zeroed by the caller)
+  float* acc_f32;
+  int64_t ld_acc;
 };
+
+// ---------------------------------------------------------------- epilogue math
+// One output of the SPLIT epilogue: y = S_a S_w (acc - zp cs) + rho kappa aux
+__device__ __forceinline__ float g2_epi_split(const G2Params& p, int col, int acc_raw, int zp,
+                                              float s_row, float rho, bool has_aux, float aux) {
+  const int acc = acc_raw - (p.row_zp ? zp * p.col_cs[col] : 0);
+  float v = s_row * p.col_s[col] * (float)acc;
+  if (has_aux) v = fmaf(rho * p.col_kappa[col], aux, v);
+  return v;
+}
+// One output of the LR1 epilogue: fp16 hi (+ lo) of (S/rho)(S_u/sigma) acc
+__device__ __forceinline__ void g2_epi_lr1(const G2Params& p, int orow, int col, int acc_raw,
+                                           int zp, float s_row) {
+  __half* o = reinterpret_cast<__half*>(p.out);
+  const int acc = acc_raw - (p.row_zp ? zp * p.col_cs[col] : 0);
+  const float v = acc == 0 ? 0.f : s_row * p.col_s[col] * (float)acc;
+  if (!(fabsf(v) <= 65504.f) && p.err) atomicOr(p.err, 8 /*ERR_LR_RANGE*/);
+  const __half hv = __float2half_rn(v);
+  o[(int64_t)orow * p.ldo + p.col_off + col] = hv;
+  if (p.lo_off) o[(int64_t)orow * p.ldo + p.col_off + p.lo_off + col] = __float2half_rn(v - __half2float(hv));
+}
+__device__ __forceinline__ void g2_store1(const G2Params& p, int64_t idx, float v) {
+  if (p.out_dtype == G2_F32) reinterpret_cast<float*>(p.out)[idx] = v;
+  else if (p.out_dtype == G2_F16) reinterpret_cast<__half*>(p.out)[idx] = __float2half_rn(v);
+  else reinterpret_cast<__nv_bfloat16*>(p.out)[idx] = __float2bfloat16_rn(v);
+}
 
 // ---------------------------------------------------------------- pair helpers
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -201,6 +237,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
   const int pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
   const int n_aux = p.k_aux / 64, n_main = g2_chunks(p.k_main);
   const int stages_per_tile = n_aux + n_main;
+  const int ksplit = p.k_split > 1 ? p.k_split : 1;
+  const int num_items = num_tiles * ksplit;
+  // work item -> (tile, stage range [s0, s1))
+  auto item_of = [&](int item, int& tile, int& s0, int& s1) {
+    tile = item / ksplit;
+    const int ks = item - tile * ksplit;
+    s0 = ks * stages_per_tile / ksplit;
+    s1 = (ks + 1) * stages_per_tile / ksplit;
+  };
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -232,10 +277,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
       const uint32_t tx = 2u * (G2_A_BYTES + (uint32_t)(p.bn / 2) * 128u);
       const uint32_t tx_a = 2u * G2_A_BYTES;               // packed main stages: A only
       const uint32_t tx_bp = (uint32_t)(p.bn / 2) * 64u;   // local packed staging box
-      for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+      for (int item = pair; item < num_items; item += num_pairs) {
+        int tile, s0, s1;
+        item_of(item, tile, s0, s1);
         const int m0 = (tile / n_tiles) * G2_BM + (int)rank * 128;
         const int n0 = (tile % n_tiles) * p.bn + (int)rank * (p.bn / 2);
-        for (int v = 0; v < stages_per_tile; ++v) {
+        for (int v = s0; v < s1; ++v) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + G2_A_BYTES;
@@ -275,7 +322,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
       uint32_t phase = 0;
       int it = 0;
       const uint32_t smem0 = smem_u32(smem);
-      for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
+      for (int item = pair; item < num_items; item += num_pairs, ++it) {
+        int tile, s0, s1;
+        item_of(item, tile, s0, s1);
+        const int first_main = s0 > n_aux ? s0 : n_aux;  // first main / aux stage of the range
         const int b = it & 1;
         const uint32_t tph = (it >> 1) & 1;
         mbar_wait(&tempty[b], tph ^ 1);
@@ -283,7 +333,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
         // with the aux accumulator: [main 128 | aux 128] per buffer; without: main bn
         const uint32_t d_main = tmem + b * (n_aux ? 256 : p.bn);
         const uint32_t d_aux = d_main + 128;
-        for (int v = 0; v < stages_per_tile; ++v) {
+        for (int v = s0; v < s1; ++v) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem0 + stage * STAGE_BYTES;
@@ -293,7 +343,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
             if (elect_one()) {
 #pragma unroll
               for (int k = 0; k < 4; ++k)  // K = 16 fp16 (32 B) per MMA
-                mma_f16_pair(d_aux, ad + 2 * k, bd + 2 * k, p.idesc_aux, (v | k) != 0);
+                mma_f16_pair(d_aux, ad + 2 * k, bd + 2 * k, p.idesc_aux, (v != s0) || k != 0);
               tc_commit_pair(&empty[stage]);
             }
           } else {
@@ -302,7 +352,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
             if (elect_one()) {
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                if (k < nk) mma_i8_pair(d_main, ad + 2 * k, bd + 2 * k, p.idesc_main, (c | k) != 0);
+                if (k < nk) mma_i8_pair(d_main, ad + 2 * k, bd + 2 * k, p.idesc_main, (v != first_main) || k != 0);
               tc_commit_pair(&empty[stage]);
             }
           }
@@ -325,8 +375,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
     if (num_tiles > 0) {
       int stage = 0, seq = 0;
       uint32_t phase = 0;
-      for (int tile = pair; tile < num_tiles; tile += num_pairs) {
-        for (int v = 0; v < stages_per_tile; ++v, ++seq) {
+      for (int item = pair; item < num_items; item += num_pairs) {
+        int tile, s0, s1;
+        item_of(item, tile, s0, s1);
+        for (int v = s0; v < s1; ++v, ++seq) {
           if ((seq & 3) == cw) {
             mbar_wait(&empty[stage], phase ^ 1);  // previous use of the slot drained
             if (v >= n_aux) {
@@ -359,9 +411,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
     const int lq = warp & 3;                 // TMEM lane quarter
     const int r_local = lq * 32 + lane;
     const uint32_t tempty_leader = mapa_shared(&tempty[0], 0);
-    const bool has_aux = p.k_aux > 0;
+    const bool aux_buf = p.k_aux > 0;  // TMEM layout has the aux half
     int it = 0;
-    for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
+    for (int item = pair; item < num_items; item += num_pairs, ++it) {
+      int tile, s0, s1;
+      item_of(item, tile, s0, s1);
+      const bool has_aux = aux_buf && s0 < n_aux;               // range touched the aux accumulator
+      const bool has_main = s1 > (s0 > n_aux ? s0 : n_aux);     // ... and the main one
       const int b = it & 1;
       const uint32_t tph = (it >> 1) & 1;
       const int m0 = (tile / n_tiles) * G2_BM + (int)rank * 128;
@@ -377,14 +433,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
         if (p.row_zp) zp = p.row_zp[row];
         if (has_aux && p.row_rho) rho = p.row_rho[row];
       }
-      const uint32_t lane_base = tmem + ((uint32_t)(lq * 32) << 16) + b * (has_aux ? 256 : p.bn);
+      const uint32_t lane_base = tmem + ((uint32_t)(lq * 32) << 16) + b * (aux_buf ? 256 : p.bn);
       for (int c0 = 0; c0 < p.bn; c0 += 32) {
         uint32_t am[32], af[32];
         tmem_ld32(lane_base + c0, am);
         if (has_aux) tmem_ld32(lane_base + 128 + c0, af);
         tmem_wait_ld();
         if (!row_ok) continue;
-        if (p.mode == G2_RAW) {
+        if (p.mode == G2_ACC) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = n0 + c0 + j;
+            if (col < p.N) {
+              const int64_t idx = (int64_t)row * p.ld_acc + col;
+              if (has_main) atomicAdd(p.acc_i32 + idx, (int)am[j]);
+              if (has_aux) atomicAdd(p.acc_f32 + idx, __uint_as_float(af[j]));
+            }
+          }
+        } else if (p.mode == G2_RAW) {
           int* o = reinterpret_cast<int*>(p.out);
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -396,18 +462,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
             }
           }
         } else if (p.mode == G2_LR1) {
-          __half* o = reinterpret_cast<__half*>(p.out);
           const int orow = p.row_map ? p.row_map[row] : row;
+          __half* o = reinterpret_cast<__half*>(p.out) + (int64_t)orow * p.ldo + p.col_off;
+          const bool vec = ((p.ldo | p.col_off | p.lo_off) & 7) == 0;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = n0 + c0 + j;
-            if (col < p.N) {
-              const int acc = (int)am[j] - (p.row_zp ? zp * p.col_cs[col] : 0);
-              const float v = acc == 0 ? 0.f : s_row * p.col_s[col] * (float)acc;
-              if (!(fabsf(v) <= 65504.f) && p.err) atomicOr(p.err, 8 /*ERR_LR_RANGE*/);
-              const __half hv = __float2half_rn(v);
-              o[(int64_t)orow * p.ldo + p.col_off + col] = hv;
-              if (p.lo_off) o[(int64_t)orow * p.ldo + p.col_off + p.lo_off + col] = __float2half_rn(v - __half2float(hv));
+          for (int g = 0; g < 32; g += 8) {
+            const int colg = n0 + c0 + g;
+            if (vec && colg + 8 <= p.N) {  // 8 columns -> one 16-byte store (+ one for lo)
+              __half hv[8], lv[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const int col = colg + j;
+                const int acc = (int)am[g + j] - (p.row_zp ? zp * p.col_cs[col] : 0);
+                const float v = acc == 0 ? 0.f : s_row * p.col_s[col] * (float)acc;
+                if (!(fabsf(v) <= 65504.f) && p.err) atomicOr(p.err, 8 /*ERR_LR_RANGE*/);
+                hv[j] = __float2half_rn(v);
+                lv[j] = __float2half_rn(v - __half2float(hv[j]));
+              }
+              *reinterpret_cast<uint4*>(o + colg) = *reinterpret_cast<const uint4*>(hv);
+              if (p.lo_off) *reinterpret_cast<uint4*>(o + p.lo_off + colg) = *reinterpret_cast<const uint4*>(lv);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (colg + j < p.N) g2_epi_lr1(p, orow, colg + j, (int)am[g + j], zp, s_row);
             }
           }
         } else {
@@ -415,10 +492,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int col = min(n0 + c0 + j, p.N - 1);
-            const int acc = (int)am[j] - (p.row_zp ? zp * p.col_cs[col] : 0);
-            float v = s_row * p.col_s[col] * (float)acc;
-            if (has_aux) v = fmaf(rho * p.col_kappa[col], __uint_as_float(af[j]), v);
-            y[j] = v;
+            y[j] = g2_epi_split(p, col, (int)am[j], zp, s_row, rho, has_aux, __uint_as_float(af[j]));
           }
           const int64_t base = (int64_t)row * p.ldo + n0 + c0;
           const bool full_chunk = (n0 + c0 + 32 <= p.N) && ((p.ldo & 7) == 0);
@@ -475,6 +549,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_pair(tmem, G2_TMEM_COLS);
+  }
+}
+
+// Finalize of a split-K (G2_ACC) launch: one thread per output element;
+// `mode` is the epilogue the single-pass kernel would have run.
+__global__ void g2_finalize_kernel(const G2Params p, int mode, int has_aux) {
+  const int M = p.m_count ? *p.m_count : p.M;
+  const int64_t total = (int64_t)M * p.N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(e / p.N), col = (int)(e - (int64_t)row * p.N);
+    const int64_t ai = (int64_t)row * p.ld_acc + col;
+    const int acc = p.acc_i32[ai];
+    const float aux = has_aux ? p.acc_f32[ai] : 0.f;
+    const float s_row = p.row_s ? p.row_s[row] : 0.f;
+    const int zp = p.row_zp ? p.row_zp[row] : 0;
+    if (mode == G2_RAW) {
+      const int64_t idx = (int64_t)row * p.ldo + col;
+      reinterpret_cast<int*>(p.out)[idx] = acc;
+      if (has_aux && p.raw_aux) p.raw_aux[idx] = aux;
+    } else if (mode == G2_LR1) {
+      g2_epi_lr1(p, p.row_map ? p.row_map[row] : row, col, acc, zp, s_row);
+    } else {
+      const float rho = (has_aux && p.row_rho) ? p.row_rho[row] : 0.f;
+      g2_store1(p, (int64_t)row * p.ldo + col, g2_epi_split(p, col, acc, zp, s_row, rho, has_aux, aux));
+    }
   }
 }
 

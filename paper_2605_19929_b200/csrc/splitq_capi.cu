@@ -148,7 +148,7 @@ struct splitq_layer_s {
   int64_t k_nat = 0;
   int64_t ld_main = 0, ld_text = 0, ld_vis = 0;
   int64_t r_s16 = 0, r_c16 = 0, k_lr = 0;  // k_lr = K of the fp16 auxiliary GEMM
-  int64_t kt16 = 0, kv16 = 0, off_t = 0, off_v = 0, off_s = 0, off_c = 0;
+  int64_t kt16 = 0, kv16 = 0, off_t = 0, off_v = 0, off_s = 0, off_c = 0, r_s8 = 0;
   DevBuf mem;
   int* c_main = nullptr; double* d_main = nullptr; float* d_main32 = nullptr;
   int k3_ok = 0;  // smoothing scales within the fp32 fast path's range
@@ -281,8 +281,11 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
   L->off_t = 0;
   L->off_v = 3 * L->kt16;
   L->off_s = L->off_v + 3 * L->kv16;
-  L->off_c = L->off_s + 2 * L->r_s;  // the fp16 MMA K step is 16 and a stage 64:
-  L->k_lr = (L->off_c + L->r_c) ? round_up(L->off_c + L->r_c, 64) : 0;  // only the total pads
+  // segments start at multiples of 8 halves (16 B: LR1 stores 8 columns at a
+  // time); the fp16 MMA K step is 16 and a stage 64, so only the total pads
+  L->r_s8 = round_up(L->r_s, 8);
+  L->off_c = L->off_s + 2 * L->r_s8;
+  L->k_lr = (L->off_c + L->r_c) ? round_up(L->off_c + L->r_c, 64) : 0;
 
   auto cleanup = [&](int code) {
     L->mem.release();
@@ -424,7 +427,7 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
       split3(L->off_t, L->n_text, L->kt16);
       split3(L->off_v, L->n_vis, L->kv16);
       for (int64_t c = 0; c < L->r_s; ++c)
-        dst[L->off_s + c] = dst[L->off_s + L->r_s + c] = __double2half(row[L->off_s + c] / kappa);
+        dst[L->off_s + c] = dst[L->off_s + L->r_s8 + c] = __double2half(row[L->off_s + c] / kappa);
       for (int64_t c = 0; c < L->r_c; ++c) dst[L->off_c + c] = __double2half(row[L->off_c + c] / kappa);
       kap[j] = (float)(kappa * colf);
     }
@@ -487,6 +490,20 @@ int splitq_workspace_layout(splitq_layer_t L, int64_t T, splitq_ws_layout_t* o) 
   }
   o->k_lr = L->k_lr;
   if (L->k_lr) o->lr_a = take(2 * T * L->k_lr);
+  {
+    // split-K scratch (int32 + fp32 partial accumulators) for launches whose
+    // tile count cannot fill the GPU (decode-sized calls); shared by the LR1
+    // and split-GEMM launches, which run in sequence on one stream
+    const int64_t pairs = sm_count(L->device) / 2;
+    const int64_t m_tiles = (T + 255) / 256;
+    int64_t need = 0;
+    const int64_t bn = std::min<int64_t>(L->k_lr ? 128 : 256, round_up(L->d_out, 32));
+    if (m_tiles * ((L->d_out + bn - 1) / bn) * 2 <= pairs) need = std::max(need, T * L->d_out * 8);
+    for (int64_t r : {L->r_s, L->r_c})
+      if (r && m_tiles * 2 <= pairs) need = std::max(need, T * r * 4);
+    o->acc_scratch_bytes = need;
+    o->acc_scratch = need ? take(need) : -1;
+  }
   o->total_bytes = off;
   o->code_centered_main = L->act.centered;
   o->main_natural = 1;
@@ -498,7 +515,6 @@ int splitq_workspace_layout(splitq_layer_t L, int64_t T, splitq_ws_layout_t* o) 
 
 namespace {
 
-bool g_gemm_attr_set[64] = {false};
 
 struct GemmLaunch {
   G2Maps maps;
@@ -508,7 +524,8 @@ struct GemmLaunch {
 // Persistent launch: one CTA pair per two SMs (cluster of 2).
 inline bool raw_unpacked(int flags) { return (flags & SPLITQ_FWD_UNPACKED) != 0; }
 
-int launch_gemm(GemmLaunch& g, int device, int64_t max_rows, cudaStream_t stream) {
+int launch_gemm(GemmLaunch& g, int device, int64_t max_rows, cudaStream_t stream,
+                void* scratch = nullptr, int64_t scratch_bytes = 0) {
   static bool attr[64][2] = {};
   const int pk = g.p.packed_b ? 1 : 0;
   if (device >= 0 && device < 64 && !attr[device][pk]) {
@@ -520,12 +537,38 @@ int launch_gemm(GemmLaunch& g, int device, int64_t max_rows, cudaStream_t stream
   const int64_t n_tiles = (g.p.N + g.p.bn - 1) / g.p.bn;
   const int64_t tiles = m_tiles * n_tiles;
   if (tiles == 0) return SPLITQ_OK;
-  const int pairs = (int)std::min<int64_t>(tiles, sm_count(device) / 2);
+  const int64_t avail = sm_count(device) / 2;
+  // Split-K when the tiles cannot fill the GPU (decode): each work item is a
+  // K range of a tile, partial sums land in the scratch with RED atomics and a
+  // finalize pass applies the epilogue.
+  const int stages = g.p.k_aux / 64 + (g.p.k_main + 127) / 128;
+  const bool has_aux = g.p.k_aux > 0;
+  const int64_t need = max_rows * g.p.N * (has_aux ? 8 : 4);
+  g.p.k_split = 1;
+  int final_mode = g.p.mode;
+  if (scratch && tiles * 2 <= avail && stages >= 2 && need <= scratch_bytes &&
+      !getenv("SPLITQ_NO_SPLITK")) {
+    g.p.k_split = (int)std::min<int64_t>(stages, std::max<int64_t>(2, avail / tiles));
+    g.p.acc_i32 = reinterpret_cast<int*>(scratch);
+    g.p.acc_f32 = reinterpret_cast<float*>(reinterpret_cast<int*>(scratch) + max_rows * g.p.N);
+    g.p.ld_acc = g.p.N;
+    g.p.mode = G2_ACC;
+    CUDA_TRY(cudaMemsetAsync(scratch, 0, need, stream));
+  }
+  const int64_t items = tiles * g.p.k_split;
+  const int pairs = (int)std::min<int64_t>(items, avail);
   if (pk)
     splitq_gemm2_kernel<true><<<2 * pairs, G2_THREADS_PACKED, G2_SMEM_BYTES, stream>>>(g.maps, g.p);
   else
     splitq_gemm2_kernel<false><<<2 * pairs, G2_THREADS, G2_SMEM_BYTES, stream>>>(g.maps, g.p);
   CUDA_TRY(cudaGetLastError());
+  if (g.p.mode == G2_ACC) {
+    const int64_t total = max_rows * g.p.N;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4L * sm_count(device));
+    g2_finalize_kernel<<<blocks, 256, 0, stream>>>(g.p, final_mode, has_aux ? 1 : 0);
+    CUDA_TRY(cudaGetLastError());
+    g.p.mode = final_mode;
+  }
   return SPLITQ_OK;
 }
 
@@ -797,12 +840,12 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
               map_i8(&g.maps.b, bu, r, L->k_nat, L->ld_main, g.p.bn / 2);
     g.maps.xa = g.maps.xb = g.maps.a;
     if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (LR1)");
-    return launch_gemm(g, L->device, T, stream);
+    return launch_gemm(g, L->device, T, stream, at(W.acc_scratch), W.acc_scratch_bytes);
   };
   if (L->r_s &&
       (rc = lr1(at(W.a_main), L->act.centered, L->b_us, L->s_us, L->cs_us, L->r_s,
                 (const float*)at(W.lrs_main), L->act.centered ? nullptr : (const int*)at(W.zp_main),
-                nullptr, nullptr, L->off_s, L->r_s)))
+                nullptr, nullptr, L->off_s, L->r_s8)))
     return rc;
   if (L->r_c &&
       (rc = lr1(at(W.a_mac), L->aux.centered, L->b_uc, L->s_uc, L->cs_uc, L->r_c,
@@ -851,7 +894,7 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
     ok = map_f16(&g.maps.xa, lr_a, T, L->k_lr, L->k_lr, 128) &&
          map_f16(&g.maps.xb, L->b_lr, L->d_out, L->k_lr, L->k_lr, g.p.bn / 2);
   if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (split GEMM)");
-  if ((rc = launch_gemm(g, L->device, T, stream))) return rc;
+  if ((rc = launch_gemm(g, L->device, T, stream, at(W.acc_scratch), W.acc_scratch_bytes))) return rc;
   if (prof && (rc = prof_record(L, stream))) return rc;
   return SPLITQ_OK;
 }

@@ -284,7 +284,13 @@ def test_packed_weights_match_int8_weights(name):
     g = runtime.packed(layer)
     xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
     td = torch.from_numpy(tags).cuda()
-    for raw in (True, False):
-        a = g.run(xd, td, raw=raw).cpu().numpy()
-        b = g.run(xd, td, raw=raw, unpacked=True).cpu().numpy()
-        np.testing.assert_array_equal(a, b)
+    # main int32 accumulators bit-exact; the fp32 auxiliary plane and the
+    # outputs agree to fp32 rounding (split-K sums them in any order)
+    a = g.run(xd, td, raw=True)
+    b = g.run(xd, td, raw=True, unpacked=True)
+    np.testing.assert_array_equal(a[0].cpu().numpy(), b[0].cpu().numpy())
+    fa, fb = a[1].view(torch.float32).cpu().numpy(), b[1].view(torch.float32).cpu().numpy()
+    np.testing.assert_allclose(fa, fb, rtol=1e-5, atol=1e-6 * np.abs(fb).max())
+    ya = g.run(xd, td).cpu().numpy()
+    yb = g.run(xd, td, unpacked=True).cpu().numpy()
+    np.testing.assert_allclose(ya, yb, rtol=1e-5, atol=1e-5 * np.abs(yb).max())
