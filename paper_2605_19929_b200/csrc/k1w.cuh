@@ -429,17 +429,18 @@ struct KwZ {
   }
 };
 
-template <typename T, bool SMZ>
+// SMF: the MAC fractions f of a text row are kept in SMEM between pass E and
+// pass G as 16-bit fixed point (f * 2^15, offset-binary), so pass G does not
+// recompute the row: the extra rounding (<= 2^-16) enters the MAC tie window
+// (kw_consts2 err_extra); rows whose window would get too wide recompute.
+template <typename T, bool SMF>
 __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d_in) {
   extern __shared__ __align__(16) uint8_t kw_smem[];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5, nwc = blockDim.x >> 5;
   const int nchunks = d_in >> 3;
   uint32_t* q = reinterpret_cast<uint32_t*>(kw_smem) + wl * KW_QCAP;
-  KwZ zs{nullptr, nullptr};
-  if (SMZ) {
-    float4* base = reinterpret_cast<float4*>(kw_smem + nwc * KW_QCAP * 4) + (size_t)wl * 2 * nchunks;
-    zs = KwZ{base, base + nchunks};
-  }
+  uint4* fs = SMF ? reinterpret_cast<uint4*>(kw_smem + nwc * KW_QCAP * 4) + (size_t)wl * nchunks
+                  : nullptr;
   const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nw = (int)((gridDim.x * blockDim.x) >> 5);
   const bool cen = p.act.centered != 0, cena = p.aux.centered != 0;
@@ -468,7 +469,6 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
         nz[2 * h] = -zz.x;
         nz[2 * h + 1] = -zz.y;
       }
-      if (SMZ) zs.put(j, z);
       kw_ext_upd(elo, kw_min8(z), j);
       kw_ext_upd(ehi, kw_min8(nz), j);
     }
@@ -516,14 +516,9 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     if (elo.m1 <= bl || ehi.m1 <= bh) {
       const bool all = elo.m2 <= bl || ehi.m2 <= bh || (elo.m1 <= bl && ehi.m1 <= bh && elo.c1 != ehi.c1);
       for (int j = all ? lane : (elo.m1 <= bl ? elo.c1 : ehi.c1); j < nchunks; j += 32) {
-        float z[8];
-        if (SMZ) {
-          zs.get(j, z);
-        } else {
-          float x[8], d[8];
-          kw_load<T>(p, xg, j, x, d);
-          kw_mulz(x, d, z);
-        }
+        float z[8], x[8], d[8];
+        kw_load<T>(p, xg, j, x, d);
+        kw_mulz(x, d, z);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           if (z[u] <= bl || -z[u] <= bh) {
@@ -610,22 +605,30 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
         const int j = j0 + lane;
         bool flag = false;
         if (j < nchunks) {
-          float z[8], v[8];
+          float z[8], v[8], x[8], d[8];
           uint32_t b[8];
-          if (SMZ) {
-            zs.get(j, z);
-          } else {
-            float x[8], d[8];
-            kw_load<T>(p, xg, j, x, d);
-            kw_mulz(x, d, z);
-          }
+          kw_load<T>(p, xg, j, x, d);
+          kw_mulz(x, d, z);
           kw_vt(z, c, v, b);
           *reinterpret_cast<uint2*>(arow + 8 * j) = kw_pack_shift(b, c.F);
           flag = kw_minfrac(b, c.fm) <= c.W2;
           if (mac) {
             float f[8], nf[8];
             kw_frac(v, b, c, f);
-            if (SMZ) zs.put(j, f);
+            if (SMF) {  // f * 2^15 rounded, offset-binary u16 (|f| < 1 off the flagged window)
+              uint32_t u[8];
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                const float2 t = kw_fma2(make_float2(f[2 * h], f[2 * h + 1]), make_float2(32768.f, 32768.f),
+                                         make_float2(12582912.f, 12582912.f));
+                u[2 * h] = __float_as_uint(t.x);
+                u[2 * h + 1] = __float_as_uint(t.y);
+              }
+              fs[j] = make_uint4(__byte_perm(u[0], u[1], 0x5410) ^ 0x80008000u,
+                                 __byte_perm(u[2], u[3], 0x5410) ^ 0x80008000u,
+                                 __byte_perm(u[4], u[5], 0x5410) ^ 0x80008000u,
+                                 __byte_perm(u[6], u[7], 0x5410) ^ 0x80008000u);
+            }
             if (!flag) {
 #pragma unroll
               for (int e = 0; e < 8; ++e) nf[e] = -f[e];
@@ -668,17 +671,12 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     if (!allx && (flo.m1 <= bfl || fhi.m1 <= bfh)) {
       const bool all = flo.m2 <= bfl || fhi.m2 <= bfh || (flo.m1 <= bfl && fhi.m1 <= bfh && flo.c1 != fhi.c1);
       for (int j = all ? lane : (flo.m1 <= bfl ? flo.c1 : fhi.c1); j < nchunks; j += 32) {
-        float f[8];
-        if (SMZ) {
-          zs.get(j, f);
-        } else {
-          float x[8], d[8], z[8], v[8];
-          uint32_t b[8];
-          kw_load<T>(p, xg, j, x, d);
-          kw_mulz(x, d, z);
-          kw_vt(z, c, v, b);
-          kw_frac(v, b, c, f);
-        }
+        float f[8], x[8], d[8], z[8], v[8];
+        uint32_t b[8];
+        kw_load<T>(p, xg, j, x, d);
+        kw_mulz(x, d, z);
+        kw_vt(z, c, v, b);
+        kw_frac(v, b, c, f);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           if (f[u] <= bfl || -f[u] <= bfh) {
@@ -696,12 +694,18 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     double Se = 1.0;
     int zpe = 0;
     float ratio = 1.f;
+    int use_smf = 0;
     if (lane == 0) {
       double rSe;
       if (!kw_params(elo64, ehi64, p.aux, &Se, &zpe, &rSe)) atomicOr(p.err, ERR_SCALE_ZERO);
-      // f carries |err| <= vmax 2^-22 in units of S: times S / Se in units of e / Se
-      ce = kw_consts2(elo64, ehi64, Se, rSe, zpe, p.aux,
-                      (double)vmaxf * 2.384185791015625e-07 * (S * rSe) * 1.01);
+      // f carries |err| <= vmax 2^-22 in units of S (+ 2^-16 when read back from
+      // the 16-bit SMEM copy): times S / Se in units of e / Se
+      const double ef = (double)vmaxf * 2.384185791015625e-07;
+      if (SMF) {
+        ce = kw_consts2(elo64, ehi64, Se, rSe, zpe, p.aux, (ef + 1.52587890625e-05) * (S * rSe) * 1.01);
+        use_smf = ce.safe && ce.W2 <= 16;
+      }
+      if (!use_smf) ce = kw_consts2(elo64, ehi64, Se, rSe, zpe, p.aux, ef * (S * rSe) * 1.01);
       p.s_mac[slot] = Se;
       p.zp_mac[slot] = zpe;
       p.lrs_mac[slot] = (float)(Se * rrho);
@@ -711,6 +715,7 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     Se = kw_shfl_d(Se, 0);
     zpe = __shfl_sync(0xffffffffu, zpe, 0);
     ratio = __shfl_sync(0xffffffffu, ratio, 0);
+    use_smf = __shfl_sync(0xffffffffu, use_smf, 0);
 
     // ------------------------------------------------ pass G: MAC residual codes
     int8_t* erow = p.a_mac + (int64_t)slot * p.ld_main;
@@ -721,26 +726,36 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
         const int j = j0 + lane;
         bool flag = false;
         if (j < nchunks) {
-          float f[8];
           uint32_t be[8];
           bool mflag = false;
-          if (SMZ) {
-            zs.get(j, f);
+          if (SMF && use_smf) {  // f from the 16-bit SMEM copy (pass-E-flagged chunks are queued)
+            const uint4 w = fs[j];
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+            const float r15 = ratio * 3.0517578125e-05f;  // ratio * 2^-15 (exact)
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const float2 n2 = kw_add2(make_float2(__uint_as_float(__byte_perm(ws[h], 0x4B40u, 0x5410)),
+                                                    __uint_as_float(__byte_perm(ws[h], 0x4B40u, 0x5432))),
+                                        make_float2(-12615680.f, -12615680.f));  // - (1.5 2^23 + 2^15)
+              const float2 t = kw_fma2(n2, make_float2(r15, r15), make_float2(ce.C, ce.C));
+              be[2 * h] = __float_as_uint(t.x);
+              be[2 * h + 1] = __float_as_uint(t.y);
+            }
           } else {
-            float x[8], d[8], z[8], v[8];
+            float f[8], x[8], d[8], z[8], v[8];
             uint32_t b[8];
             kw_load<T>(p, xg, j, x, d);
             kw_mulz(x, d, z);
             kw_vt(z, c, v, b);
             kw_frac(v, b, c, f);
             mflag = kw_minfrac(b, c.fm) <= c.W2;
-          }
 #pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const float2 t = kw_fma2(make_float2(f[2 * h], f[2 * h + 1]), make_float2(ratio, ratio),
-                                     make_float2(ce.C, ce.C));
-            be[2 * h] = __float_as_uint(t.x);
-            be[2 * h + 1] = __float_as_uint(t.y);
+            for (int h = 0; h < 4; ++h) {
+              const float2 t = kw_fma2(make_float2(f[2 * h], f[2 * h + 1]), make_float2(ratio, ratio),
+                                       make_float2(ce.C, ce.C));
+              be[2 * h] = __float_as_uint(t.x);
+              be[2 * h + 1] = __float_as_uint(t.y);
+            }
           }
           *reinterpret_cast<uint2*>(erow + 8 * j) = kw_pack_shift(be, ce.F);
           flag = mflag || kw_minfrac(be, ce.fm) <= ce.W2;
@@ -761,8 +776,8 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
   }
 }
 
-inline size_t k1w_smem(int d_in, int warps, bool smz) {
-  return (size_t)warps * (KW_QCAP * 4 + (smz ? (size_t)d_in * 4 : 0));
+inline size_t k1w_smem(int d_in, int warps, bool smf) {
+  return (size_t)warps * (KW_QCAP * 4 + (smf ? (size_t)d_in * 2 : 0));
 }
 
 }  // namespace splitq

@@ -642,34 +642,34 @@ int launch_k1_dt(const K1Params& k, int d_in, cudaStream_t s) {
 
 // K1 warp-per-row (fp16 / bf16 rows, d_in % 8 == 0, 16-B aligned rows):
 // fp32 fast path with certified exact fp64 fallback (k1w.cuh).
-template <typename T, bool SMZ>
+template <typename T, bool SMF>
 int launch_k1w_t(const K1Params& k, int d_in, int device, cudaStream_t stream) {
-  // SMZ: one warp per CTA holding its row's z / f in SMEM; else 4 row warps per CTA
-  const int threads = SMZ ? 32 : KW_THREADS;
-  const size_t smem = k1w_smem(d_in, threads / 32, SMZ);
+  const int threads = KW_THREADS;
+  const size_t smem = k1w_smem(d_in, threads / 32, SMF);
   static int attr_dev[64] = {0};
   if (device >= 0 && device < 64 && !attr_dev[device]) {
-    CUDA_TRY(cudaFuncSetAttribute(k1w_kernel<T, SMZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_TRY(cudaFuncSetAttribute(k1w_kernel<T, SMF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   200 * 1024));
     attr_dev[device] = 1;
   }
   int per_sm = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1w_kernel<T, SMZ>, threads, smem));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1w_kernel<T, SMF>, threads, smem));
   if (per_sm < 1) return SPLITQ_ERR_UNSUPPORTED;
   const int64_t warps = (int64_t)per_sm * sm_count(device) * (threads / 32);
   const int64_t grid = (std::min<int64_t>(k.T, warps) + threads / 32 - 1) / (threads / 32);
-  k1w_kernel<T, SMZ><<<(unsigned)grid, threads, smem, stream>>>(k, d_in);
+  k1w_kernel<T, SMF><<<(unsigned)grid, threads, smem, stream>>>(k, d_in);
   CUDA_TRY(cudaGetLastError());
   return SPLITQ_OK;
 }
 
 template <typename T>
 int launch_k1w(const K1Params& k, int d_in, int device, cudaStream_t stream) {
-  static const char* env = getenv("SPLITQ_K1_SMZ");
-  // SMEM-staged z / f saves the recompute but caps residency at ~15 warps /
-  // SM; the recompute variant measured faster (0.80 vs 1.00 ms, 7B q-proj)
-  const bool smz = env ? env[0] == '1' : false;
-  return smz ? launch_k1w_t<T, true>(k, d_in, device, stream)
+  // 16-bit MAC fractions in SMEM (2 B per channel per warp): opt-in. It
+  // removes the pass-G recompute but widens the MAC tie window; measured
+  // 0.756 vs 0.696 ms on the 7B q-proj input, so the recompute stays default.
+  static const char* env = getenv("SPLITQ_K1_SMF");
+  const bool smf = k.use_mac && env && env[0] == '1' && d_in <= 8192;
+  return smf ? launch_k1w_t<T, true>(k, d_in, device, stream)
              : launch_k1w_t<T, false>(k, d_in, device, stream);
 }
 
