@@ -17,6 +17,12 @@
 // (leader CTA only), 2..5 epilogue, 6..9 weight unpack. Accumulators are
 // double-buffered so the epilogue of tile t overlaps the MMAs of tile t+1.
 //
+// Swap-AB (p.swap, decode-sized token counts): the 256-row MMA tile runs over
+// output channels (A = weights [N x K], B = token codes [M x K], both K-major
+// as stored) and the tile's N over tokens, so a 16..64-token call does not pad
+// the MMA to 256 token rows. TMEM lane = output channel, column = token; the
+// epilogue swaps the row / column roles of the scales.
+//
 // Packed weights (p.packed_b): the main B operand lives in HBM as 4-bit
 // two's-complement codes (W4, and W3 in the same container), two per byte,
 // interleaved so that byte i of each 32-bit word holds codes 8g+i (low nibble)
@@ -51,21 +57,21 @@ constexpr int G2_SMEM_BYTES = G2_RING_BYTES + 1024 + 512;
 
 // stage geometry for a tile width: per CTA an A box (128 x 128 B), a B box
 // (bn/2 x 128 B) and, with packed weights, the packed staging box (bn/2 x 64 B)
-__host__ __device__ inline int g2_stage_bytes(int bn, int packed) {
-  return G2_A_BYTES + bn * 64 + (packed ? bn * 32 : 0);
+__host__ __device__ inline int g2_stage_bytes(int bn, int packed, int swap = 0) {
+  return G2_A_BYTES + bn * 64 + (packed ? (swap ? 128 * 64 : bn * 32) : 0);
 }
-__host__ __device__ inline int g2_stages(int bn, int packed) {
-  const int s = G2_RING_BYTES / g2_stage_bytes(bn, packed);
+__host__ __device__ inline int g2_stages(int bn, int packed, int swap = 0) {
+  const int s = G2_RING_BYTES / g2_stage_bytes(bn, packed, swap);
   return s < G2_MAX_STAGES ? s : G2_MAX_STAGES;
 }
 
 enum G2Mode : int { G2_SPLIT = 0, G2_RAW = 1, G2_LR1 = 2, G2_ACC = 3 };
-// G2_ACC (split-K): work item = (tile, K range); the epilogue adds the int32
-// main / fp32 aux partial accumulators into acc_i32 / acc_f32 [rows x ld_acc]
-// with RED atomics, and g2_finalize_* apply the SPLIT / LR1 / RAW epilogue
-// (same arithmetic, g2_epi_*) once every range has landed. The int32 sum is
-// exact in any order; the fp32 auxiliary sum is order-dependent in its last
-// bits only.
+// G2_ACC (split-K): work item = (tile, K range ks); the epilogue stores the
+// int32 main / fp32 aux partial accumulators of range ks into its own slice
+// acc_i32 / acc_f32 + ks * slice [rows x ld_acc] (plain coalesced stores, no
+// atomics; ranges that did not touch an accumulator store zeros), and
+// g2_finalize_kernel sums the slices in range order and applies the SPLIT /
+// LR1 / RAW epilogue (same arithmetic, g2_epi_*): deterministic.
 enum G2Out : int { G2_F32 = 0, G2_F16 = 1, G2_BF16 = 2 };
 
 struct G2Maps {
@@ -82,7 +88,8 @@ struct G2Params {
   int k_aux;          // fp16 K (multiple of 64; 0 = no aux branch)
   uint32_t idesc_main, idesc_aux;
   int mode, out_dtype;
-  int packed_b;         // main B operand as packed 4-bit codes (see header)
+  int packed_b;         // weights as packed 4-bit codes (see header)
+  int swap;             // swap-AB: tile rows = output channels, tile cols = tokens
   const float* row_s;   // S_a (SPLIT) or S/rho (LR1)
   const int* row_zp;    // zero points when A codes are u8
   const float* row_rho;
@@ -97,9 +104,11 @@ struct G2Params {
   float* raw_aux;       // RAW: fp32 aux plane
   int* err;
   int k_split;          // >= 1: K ranges per tile (G2_ACC when > 1)
-  int* acc_i32;         // G2_ACC scratch (zeroed by the caller)
+  unsigned long long* trace;  // G2_TRACE builds: per-CTA phase timestamps (ns)
+  int* acc_i32;         // G2_ACC scratch: k_split slices of [rows x ld_acc]
   float* acc_f32;
   int64_t ld_acc;
+  int64_t acc_slice;    // elements per slice
 };
 
 // ---------------------------------------------------------------- epilogue math
@@ -211,15 +220,31 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
+__device__ __forceinline__ unsigned long long g2_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#ifdef G2_TRACE
+#define G2_STAMP(slot) do { if (p.trace) p.trace[blockIdx.x * 8 + (slot)] = g2_now(); } while (0)
+#else
+#define G2_STAMP(slot) do { } while (0)
+#endif
+
 template <bool PACKED>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_PACKED : G2_THREADS, 1)
     splitq_gemm2_kernel(const __grid_constant__ G2Maps maps, const G2Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  const int STAGES = g2_stages(p.bn, PACKED);
-  const int STAGE_BYTES = g2_stage_bytes(p.bn, PACKED);
+  const int STAGES = g2_stages(p.bn, PACKED, p.swap);
+  const int STAGE_BYTES = g2_stage_bytes(p.bn, PACKED, p.swap);
   const int B_BYTES = p.bn * 64;  // per CTA: bn/2 rows x 128 B
+  // the slot the weights land in (A with swap-AB, else B), its rows per CTA,
+  // and where the packed staging box sits in the stage
+  const int W_OFF = p.swap ? 0 : G2_A_BYTES;
+  const int W_ROWS = p.swap ? 128 : p.bn / 2;
+  const int STG_OFF = G2_A_BYTES + B_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + G2_RING_BYTES);
   uint64_t* empty = full + G2_MAX_STAGES;
   uint64_t* bfull = empty + G2_MAX_STAGES;  // packed staging landed (local)
@@ -231,8 +256,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int M = p.m_count ? *p.m_count : p.M;
-  const int m_tiles = (M + G2_BM - 1) / G2_BM;
-  const int n_tiles = (p.N + p.bn - 1) / p.bn;
+  // tile grid: 256-row MMA tiles over tokens (or over output channels, swap)
+  const int m_tiles = ((p.swap ? p.N : M) + G2_BM - 1) / G2_BM;
+  const int n_tiles = ((p.swap ? M : p.N) + p.bn - 1) / p.bn;
   const int num_tiles = m_tiles * n_tiles;
   const int pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
   const int n_aux = p.k_aux / 64, n_main = g2_chunks(p.k_main);
@@ -247,6 +273,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
     s1 = (ks + 1) * stages_per_tile / ksplit;
   };
 
+  if (threadIdx.x == 0) G2_STAMP(0);  // kernel start
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], PACKED ? 3 : 1);  // producer (A tx) [+ one unpack arrival per CTA]
@@ -264,6 +291,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) G2_STAMP(1);  // setup done (barriers, TMEM, cluster sync)
 
   if (warp == 0) {
     // ================================================== TMA producer (both CTAs)
@@ -275,8 +303,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t tx = 2u * (G2_A_BYTES + (uint32_t)(p.bn / 2) * 128u);
-      const uint32_t tx_a = 2u * G2_A_BYTES;               // packed main stages: A only
-      const uint32_t tx_bp = (uint32_t)(p.bn / 2) * 64u;   // local packed staging box
+      // packed main stages: only the activation slot comes through the pair TMA
+      const uint32_t tx_a = p.swap ? 2u * (uint32_t)(p.bn / 2) * 128u : 2u * G2_A_BYTES;
+      const uint32_t tx_bp = (uint32_t)W_ROWS * 64u;       // local packed staging box
       for (int item = pair; item < num_items; item += num_pairs) {
         int tile, s0, s1;
         item_of(item, tile, s0, s1);
@@ -291,19 +320,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
             if (leader) mbar_arrive_expect_tx(&full[stage], pk ? tx_a : tx);
             // bfull advances once per ring slot use (packed: with the staging
             // bytes; otherwise a plain arrival) so its phase stays in lockstep
-            // with the ring phase the unpack warps wait on
+            // with the ring phase the unpack warps wait on.
+            // swap-AB: the A slot takes the weight rows (m0), B the token rows (n0)
+            const CUtensorMap* am = p.swap ? &maps.b : &maps.a;   // A-slot operand, main
+            const CUtensorMap* bm = p.swap ? &maps.a : &maps.b;
+            const CUtensorMap* axm = p.swap ? &maps.xb : &maps.xa;  // aux
+            const CUtensorMap* bxm = p.swap ? &maps.xa : &maps.xb;
             if (v < n_aux) {
-              tma_load_2d_pair(sa, &maps.xa, &full[stage], v * 64, m0);
-              tma_load_2d_pair(sb, &maps.xb, &full[stage], v * 64, n0);
+              tma_load_2d_pair(sa, axm, &full[stage], v * 64, m0);
+              tma_load_2d_pair(sb, bxm, &full[stage], v * 64, n0);
               if (PACKED) mbar_arrive(&bfull[stage]);
             } else {
               const int c = v - n_aux;
-              tma_load_2d_pair(sa, &maps.a, &full[stage], c * 128, m0);
               if (pk) {
+                // activations through the pair TMA; packed weights to the local staging box
+                if (p.swap) tma_load_2d_pair(sb, &maps.a, &full[stage], c * 128, n0);
+                else tma_load_2d_pair(sa, &maps.a, &full[stage], c * 128, m0);
                 mbar_arrive_expect_tx(&bfull[stage], tx_bp);
-                tma_load_2d(sb + B_BYTES, &maps.b, &bfull[stage], c * 64, n0);
+                tma_load_2d(sa + STG_OFF, &maps.b, &bfull[stage], c * 64, p.swap ? m0 : n0);
               } else {
-                tma_load_2d_pair(sb, &maps.b, &full[stage], c * 128, n0);
+                tma_load_2d_pair(sa, am, &full[stage], c * 128, m0);
+                tma_load_2d_pair(sb, bm, &full[stage], c * 128, n0);
                 if (PACKED) mbar_arrive(&bfull[stage]);
               }
             }
@@ -336,6 +373,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
         for (int v = s0; v < s1; ++v) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+          if (lane == 0 && v == s0 && it == 0) G2_STAMP(2);  // first stage's data ready
           const uint32_t a_addr = smem0 + stage * STAGE_BYTES;
           const uint64_t ad = sw128_kmajor_desc(a_addr);
           const uint64_t bd = sw128_kmajor_desc(a_addr + G2_A_BYTES);
@@ -361,47 +399,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
         }
         if (elect_one()) tc_commit_pair(&tfull[b]);
         __syncwarp();
+        if (lane == 0) G2_STAMP(3);  // last MMA issued
       }
     }
   } else if (PACKED && warp >= G2_CONV_WARP0) {
     // ================================================== weight unpack (warps 6..9, both CTAs)
-    // Ring slots are dealt round-robin to the four unpack warps, so up to four
-    // slots are being unpacked at once; each warp unpacks a whole slot
-    // (bn/2 rows x 8 16-byte chunks) and its lane 0 arrives on the leader's
-    // full barrier for that slot (one arrival per CTA).
-    const int cw = warp - G2_CONV_WARP0;
+    // All 128 unpack threads share each ring slot (W_ROWS x 8 16-byte chunks),
+    // then one thread arrives on the leader's full barrier for this CTA.
+    const int ct = threadIdx.x - 32 * G2_CONV_WARP0;  // 0..127
     const uint32_t full_leader = mapa_shared(&full[0], 0);
-    const int outs = (p.bn / 2) * 8;  // 16-byte output chunks per slot
+    const int outs = W_ROWS * 8;  // 16-byte output chunks per slot
     if (num_tiles > 0) {
-      int stage = 0, seq = 0;
+      int stage = 0;
       uint32_t phase = 0;
       for (int item = pair; item < num_items; item += num_pairs) {
         int tile, s0, s1;
         item_of(item, tile, s0, s1);
-        for (int v = s0; v < s1; ++v, ++seq) {
-          if ((seq & 3) == cw) {
-            mbar_wait(&empty[stage], phase ^ 1);  // previous use of the slot drained
-            if (v >= n_aux) {
-              mbar_wait(&bfull[stage], phase);
-              uint8_t* sb = smem + stage * STAGE_BYTES + G2_A_BYTES;
-              const uint8_t* sp = sb + B_BYTES;
+        for (int v = s0; v < s1; ++v) {
+          mbar_wait(&empty[stage], phase ^ 1);  // previous use of the slot drained
+          if (v >= n_aux) {
+            mbar_wait(&bfull[stage], phase);
+            uint8_t* sb = smem + stage * STAGE_BYTES + W_OFF;
+            const uint8_t* sp = smem + stage * STAGE_BYTES + STG_OFF;
 #pragma unroll 4
-              for (int o = lane; o < outs; o += 32) {
-                const int r = o >> 3, c = o & 7;
-                const uint2 w = *reinterpret_cast<const uint2*>(sp + r * 64 + c * 8);
-                const uint32_t w0h = w.x >> 4, w1h = w.y >> 4;
-                uint4 out;  // sign-extend 4-bit codes: (v & 0x0F..) | ((v & 0x08..) * 0x1E)
-                out.x = (w.x & 0x0F0F0F0Fu) | ((w.x & 0x08080808u) * 0x1Eu);
-                out.y = (w0h & 0x0F0F0F0Fu) | ((w0h & 0x08080808u) * 0x1Eu);
-                out.z = (w.y & 0x0F0F0F0Fu) | ((w.y & 0x08080808u) * 0x1Eu);
-                out.w = (w1h & 0x0F0F0F0Fu) | ((w1h & 0x08080808u) * 0x1Eu);
-                *reinterpret_cast<uint4*>(sb + r * 128 + ((c ^ (r & 7)) << 4)) = out;
-              }
-              fence_proxy_async();  // generic-proxy SMEM writes -> async proxy (UMMA)
+            for (int o = ct; o < outs; o += 128) {
+              const int r = o >> 3, c = o & 7;
+              const uint2 w = *reinterpret_cast<const uint2*>(sp + r * 64 + c * 8);
+              const uint32_t w0h = w.x >> 4, w1h = w.y >> 4;
+              uint4 out;  // sign-extend 4-bit codes: (v & 0x0F..) | ((v & 0x08..) * 0x1E)
+              out.x = (w.x & 0x0F0F0F0Fu) | ((w.x & 0x08080808u) * 0x1Eu);
+              out.y = (w0h & 0x0F0F0F0Fu) | ((w0h & 0x08080808u) * 0x1Eu);
+              out.z = (w.y & 0x0F0F0F0Fu) | ((w.y & 0x08080808u) * 0x1Eu);
+              out.w = (w1h & 0x0F0F0F0Fu) | ((w1h & 0x08080808u) * 0x1Eu);
+              *reinterpret_cast<uint4*>(sb + r * 128 + ((c ^ (r & 7)) << 4)) = out;
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive_remote(full_leader + (uint32_t)(stage * sizeof(uint64_t)));
+            fence_proxy_async();  // generic-proxy SMEM writes -> async proxy (UMMA)
           }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (ct == 0) mbar_arrive_remote(full_leader + (uint32_t)(stage * sizeof(uint64_t)));
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -422,10 +457,93 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
       const uint32_t tph = (it >> 1) & 1;
       const int m0 = (tile / n_tiles) * G2_BM + (int)rank * 128;
       const int n0 = (tile % n_tiles) * p.bn;
+      if (p.swap) {
+        // ---- swap-AB: TMEM lane = output channel j, column = token i
+        const int j = m0 + r_local;
+        const bool j_ok = j < p.N;
+        mbar_wait(&tfull[b], tph);
+        tc_fence_after();
+        if (warp == 2 && lane == 0 && it == 0) G2_STAMP(6);  // accumulator ready
+        const uint32_t lb = tmem + ((uint32_t)(lq * 32) << 16) + b * (aux_buf ? 256 : p.bn);
+        // per-channel constants once; per-token ones loaded by lane jj of the
+        // chunk and broadcast with shuffles (no per-element global loads)
+        const float sw_j = j_ok && p.col_s ? p.col_s[j] : 0.f;
+        const int cs_j = j_ok && p.row_zp && p.col_cs ? p.col_cs[j] : 0;
+        const float kap_j = j_ok && has_aux && p.col_kappa ? p.col_kappa[j] : 0.f;
+        const bool lr1 = p.mode == G2_LR1;
+        __half* lo_out = reinterpret_cast<__half*>(p.out);
+        for (int c0 = 0; c0 < p.bn; c0 += 32) {
+          uint32_t am[32], af[32];
+          tmem_ld32(lb + c0, am);
+          if (has_aux) tmem_ld32(lb + 128 + c0, af);
+          tmem_wait_ld();
+          const int il = n0 + c0 + lane;
+          const bool il_ok = il < M;
+          const float s_l = il_ok && p.row_s ? p.row_s[il] : 0.f;
+          const int zp_l = il_ok && p.row_zp ? p.row_zp[il] : 0;
+          const float rho_l = il_ok && has_aux && p.row_rho ? p.row_rho[il] : 0.f;
+          const int orow_l = il_ok && p.row_map ? p.row_map[il] : il;
+          // one compact unrolled loop per mode (a single loop with every mode
+          // inside unrolls to ~5.7k instructions and thrashes the i-cache)
+          const int nrem = M - (n0 + c0);  // valid tokens in this chunk (may exceed 32)
+          if (p.mode == G2_ACC) {
+            const int64_t base = (int64_t)(item % ksplit) * p.acc_slice + (int64_t)(n0 + c0) * p.ld_acc + j;
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) {
+              if (j_ok && jj < nrem) {
+                p.acc_i32[base + (int64_t)jj * p.ld_acc] = has_main ? (int)am[jj] : 0;
+                if (aux_buf) p.acc_f32[base + (int64_t)jj * p.ld_acc] = has_aux ? __uint_as_float(af[jj]) : 0.f;
+              }
+            }
+          } else if (p.mode == G2_RAW) {
+            const int64_t base = (int64_t)(n0 + c0) * p.ldo + j;
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) {
+              if (j_ok && jj < nrem) {
+                reinterpret_cast<int*>(p.out)[base + (int64_t)jj * p.ldo] = (int)am[jj];
+                if (has_aux && p.raw_aux) p.raw_aux[base + (int64_t)jj * p.ldo] = __uint_as_float(af[jj]);
+              }
+            }
+          } else if (lr1) {  // g2_epi_lr1 with the constants hoisted
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) {
+              const float s_i = __shfl_sync(0xffffffffu, s_l, jj);
+              const int zp_i = __shfl_sync(0xffffffffu, zp_l, jj);
+              const int orow_i = __shfl_sync(0xffffffffu, orow_l, jj);
+              if (j_ok && jj < nrem) {
+                const int a2 = (int)am[jj] - zp_i * cs_j;
+                const float v = a2 == 0 ? 0.f : s_i * sw_j * (float)a2;
+                if (!(fabsf(v) <= 65504.f) && p.err) atomicOr(p.err, 8 /*ERR_LR_RANGE*/);
+                const __half hv = __float2half_rn(v);
+                __half* o = lo_out + (int64_t)orow_i * p.ldo + p.col_off + j;
+                o[0] = hv;
+                if (p.lo_off) o[p.lo_off] = __float2half_rn(v - __half2float(hv));
+              }
+            }
+          } else {  // g2_epi_split with the constants hoisted
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) {
+              const float s_i = __shfl_sync(0xffffffffu, s_l, jj);
+              const int zp_i = __shfl_sync(0xffffffffu, zp_l, jj);
+              const float rho_i = __shfl_sync(0xffffffffu, rho_l, jj);
+              if (j_ok && jj < nrem) {
+                float v = s_i * sw_j * (float)((int)am[jj] - zp_i * cs_j);
+                if (has_aux) v = fmaf(rho_i * kap_j, __uint_as_float(af[jj]), v);
+                g2_store1(p, (int64_t)(n0 + c0 + jj) * p.ldo + j, v);
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(b * sizeof(uint64_t)));
+        continue;
+      }
       const int row = m0 + r_local;
       const bool row_ok = row < M;
       mbar_wait(&tfull[b], tph);
       tc_fence_after();
+      if (warp == 2 && lane == 0 && it == 0) G2_STAMP(6);  // accumulator ready
       float s_row = 0.f, rho = 0.f;
       int zp = 0;
       if (row_ok) {
@@ -441,13 +559,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
         tmem_wait_ld();
         if (!row_ok) continue;
         if (p.mode == G2_ACC) {
+          const int64_t so = (int64_t)(item % ksplit) * p.acc_slice;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int col = n0 + c0 + j;
             if (col < p.N) {
-              const int64_t idx = (int64_t)row * p.ld_acc + col;
-              if (has_main) atomicAdd(p.acc_i32 + idx, (int)am[j]);
-              if (has_aux) atomicAdd(p.acc_f32 + idx, __uint_as_float(af[j]));
+              const int64_t idx = so + (int64_t)row * p.ld_acc + col;
+              p.acc_i32[idx] = has_main ? (int)am[j] : 0;
+              if (aux_buf) p.acc_f32[idx] = has_aux ? __uint_as_float(af[j]) : 0.f;
             }
           }
         } else if (p.mode == G2_RAW) {
@@ -544,12 +663,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
     }
   }
 
+  if (warp == 2 && lane == 0) G2_STAMP(4);  // epilogue done (this CTA)
   tc_fence_before();
   cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_pair(tmem, G2_TMEM_COLS);
   }
+  if (threadIdx.x == 0) G2_STAMP(5);  // kernel end
 }
 
 // Finalize of a split-K (G2_ACC) launch: one thread per output element;
@@ -561,8 +682,12 @@ __global__ void g2_finalize_kernel(const G2Params p, int mode, int has_aux) {
        e += (int64_t)gridDim.x * blockDim.x) {
     const int row = (int)(e / p.N), col = (int)(e - (int64_t)row * p.N);
     const int64_t ai = (int64_t)row * p.ld_acc + col;
-    const int acc = p.acc_i32[ai];
-    const float aux = has_aux ? p.acc_f32[ai] : 0.f;
+    int acc = 0;
+    float aux = 0.f;
+    for (int ks = 0; ks < p.k_split; ++ks) {  // fixed order: deterministic sums
+      acc += p.acc_i32[ks * p.acc_slice + ai];
+      if (has_aux) aux += p.acc_f32[ks * p.acc_slice + ai];
+    }
     const float s_row = p.row_s ? p.row_s[row] : 0.f;
     const int zp = p.row_zp ? p.row_zp[row] : 0;
     if (mode == G2_RAW) {

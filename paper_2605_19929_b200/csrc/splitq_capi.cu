@@ -46,6 +46,12 @@ int fail(int code, const char* fmt, ...) {
 
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
+// calls with at most this many token rows run the GEMMs swap-AB (decode)
+constexpr int64_t kSwapMaxRows = 128;
+inline bool use_swap(int64_t T) { return T <= kSwapMaxRows && !getenv("SPLITQ_NO_SWAP"); }
+// token tile of a swap-AB launch: N of the MMA (multiple of 16, <= 128)
+inline int swap_bn(int64_t T) { return (int)std::min<int64_t>(128, std::max<int64_t>(16, (T + 15) / 16 * 16)); }
+
 int sm_count(int device) {
   static int cache[64] = {0};
   if (device < 0 || device >= 64) return 148;
@@ -498,9 +504,12 @@ int splitq_workspace_layout(splitq_layer_t L, int64_t T, splitq_ws_layout_t* o) 
     const int64_t m_tiles = (T + 255) / 256;
     int64_t need = 0;
     const int64_t bn = std::min<int64_t>(L->k_lr ? 128 : 256, round_up(L->d_out, 32));
-    if (m_tiles * ((L->d_out + bn - 1) / bn) * 2 <= pairs) need = std::max(need, T * L->d_out * 8);
+    const bool swap = T <= kSwapMaxRows;
+    const int64_t kmax = 8;  // split-K slices the scratch holds
+    if (swap || m_tiles * ((L->d_out + bn - 1) / bn) * 2 <= pairs)
+      need = std::max(need, kmax * T * L->d_out * 8);
     for (int64_t r : {L->r_s, L->r_c})
-      if (r && m_tiles * 2 <= pairs) need = std::max(need, T * r * 4);
+      if (r && (swap || m_tiles * 2 <= pairs)) need = std::max(need, kmax * T * r * 4);
     o->acc_scratch_bytes = need;
     o->acc_scratch = need ? take(need) : -1;
   }
@@ -524,6 +533,9 @@ struct GemmLaunch {
 // Persistent launch: one CTA pair per two SMs (cluster of 2).
 inline bool raw_unpacked(int flags) { return (flags & SPLITQ_FWD_UNPACKED) != 0; }
 
+unsigned long long* g2_trace_last = nullptr;
+int g2_trace_ctas = 0;
+
 int launch_gemm(GemmLaunch& g, int device, int64_t max_rows, cudaStream_t stream,
                 void* scratch = nullptr, int64_t scratch_bytes = 0) {
   static bool attr[64][2] = {};
@@ -533,8 +545,8 @@ int launch_gemm(GemmLaunch& g, int device, int64_t max_rows, cudaStream_t stream
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, G2_SMEM_BYTES));
     attr[device][pk] = true;
   }
-  const int64_t m_tiles = (max_rows + G2_BM - 1) / G2_BM;
-  const int64_t n_tiles = (g.p.N + g.p.bn - 1) / g.p.bn;
+  const int64_t m_tiles = ((g.p.swap ? g.p.N : max_rows) + G2_BM - 1) / G2_BM;
+  const int64_t n_tiles = ((g.p.swap ? max_rows : g.p.N) + g.p.bn - 1) / g.p.bn;
   const int64_t tiles = m_tiles * n_tiles;
   if (tiles == 0) return SPLITQ_OK;
   const int64_t avail = sm_count(device) / 2;
@@ -543,20 +555,31 @@ int launch_gemm(GemmLaunch& g, int device, int64_t max_rows, cudaStream_t stream
   // finalize pass applies the epilogue.
   const int stages = g.p.k_aux / 64 + (g.p.k_main + 127) / 128;
   const bool has_aux = g.p.k_aux > 0;
-  const int64_t need = max_rows * g.p.N * (has_aux ? 8 : 4);
+  const int64_t slice = max_rows * g.p.N;
   g.p.k_split = 1;
   int final_mode = g.p.mode;
-  if (scratch && tiles * 2 <= avail && stages >= 2 && need <= scratch_bytes &&
-      !getenv("SPLITQ_NO_SPLITK")) {
-    g.p.k_split = (int)std::min<int64_t>(stages, std::max<int64_t>(2, avail / tiles));
-    g.p.acc_i32 = reinterpret_cast<int*>(scratch);
-    g.p.acc_f32 = reinterpret_cast<float*>(reinterpret_cast<int*>(scratch) + max_rows * g.p.N);
-    g.p.ld_acc = g.p.N;
-    g.p.mode = G2_ACC;
-    CUDA_TRY(cudaMemsetAsync(scratch, 0, need, stream));
+  if (scratch && tiles * 2 <= avail && stages >= 2 && !getenv("SPLITQ_NO_SPLITK")) {
+    int ks = (int)std::min<int64_t>(stages, std::max<int64_t>(2, avail / tiles));
+    while (ks > 1 && ks * slice * (has_aux ? 8 : 4) > scratch_bytes) --ks;  // slices must fit
+    if (ks > 1) {
+      g.p.k_split = ks;
+      g.p.acc_i32 = reinterpret_cast<int*>(scratch);
+      g.p.acc_f32 = reinterpret_cast<float*>(reinterpret_cast<int*>(scratch) + ks * slice);
+      g.p.ld_acc = g.p.N;
+      g.p.acc_slice = slice;
+      g.p.mode = G2_ACC;
+    }
   }
   const int64_t items = tiles * g.p.k_split;
   const int pairs = (int)std::min<int64_t>(items, avail);
+#ifdef G2_TRACE
+  static unsigned long long* trace_buf = nullptr;
+  if (!trace_buf) cudaMalloc(&trace_buf, 148 * 8 * 8);
+  cudaMemsetAsync(trace_buf, 0, 148 * 8 * 8, stream);
+  g.p.trace = trace_buf;
+  g2_trace_last = trace_buf;
+  g2_trace_ctas = 2 * pairs;
+#endif
   if (pk)
     splitq_gemm2_kernel<true><<<2 * pairs, G2_THREADS_PACKED, G2_SMEM_BYTES, stream>>>(g.maps, g.p);
   else
@@ -819,12 +842,14 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
                  const int* csu, int64_t r, const float* row_s, const int* row_zp,
                  const int* m_count, const int* row_map, int64_t col_off, int64_t lo_off) -> int {
     GemmLaunch g{};
+    const bool sw = use_swap(T);
     g.p.M = (int)T;
     g.p.m_count = m_count;
     g.p.N = (int)r;
-    g.p.bn = tile_n(r, false);
+    g.p.swap = sw;
+    g.p.bn = sw ? swap_bn(T) : tile_n(r, false);
     g.p.k_main = (int)L->k_nat;
-    g.p.idesc_main = idesc_i8(a_signed, g.p.bn);
+    g.p.idesc_main = sw ? make_idesc(2, 1, a_signed ? 1u : 0u, G2_BM, g.p.bn) : idesc_i8(a_signed, g.p.bn);
     g.p.mode = G2_LR1;
     g.p.row_s = row_s;
     g.p.row_zp = row_zp;
@@ -836,8 +861,9 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
     g.p.lo_off = (int)lo_off;
     g.p.row_map = row_map;
     g.p.err = err;
-    bool ok = map_i8(&g.maps.a, a_codes, T, L->k_nat, L->ld_main, 128) &&
-              map_i8(&g.maps.b, bu, r, L->k_nat, L->ld_main, g.p.bn / 2);
+    // swap-AB: the A slot (128 rows per CTA) takes the weights, B the token rows
+    bool ok = map_i8(&g.maps.a, a_codes, T, L->k_nat, L->ld_main, sw ? g.p.bn / 2 : 128) &&
+              map_i8(&g.maps.b, bu, r, L->k_nat, L->ld_main, sw ? 128 : g.p.bn / 2);
     g.maps.xa = g.maps.xb = g.maps.a;
     if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (LR1)");
     return launch_gemm(g, L->device, T, stream, at(W.acc_scratch), W.acc_scratch_bytes);
@@ -856,12 +882,15 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
 
   // ---- split GEMM: int8 main GEMM + fp16 auxiliary GEMM + merge epilogue
   GemmLaunch g{};
+  const bool sw = use_swap(T);  // decode-sized: 256-row tiles over output channels
   g.p.M = (int)T;
   g.p.N = (int)L->d_out;
-  g.p.bn = tile_n(L->d_out, L->k_lr > 0);
+  g.p.swap = sw;
+  g.p.bn = sw ? swap_bn(T) : tile_n(L->d_out, L->k_lr > 0);
   g.p.k_main = (int)L->k_nat;
   g.p.k_aux = (int)L->k_lr;
-  g.p.idesc_main = idesc_i8(L->act.centered, g.p.bn);
+  g.p.idesc_main = sw ? make_idesc(2, 1, L->act.centered ? 1u : 0u, G2_BM, g.p.bn)
+                      : idesc_i8(L->act.centered, g.p.bn);
   g.p.idesc_aux = idesc_f16(g.p.bn);
   g.p.mode = raw ? G2_RAW : G2_SPLIT;
   g.p.out_dtype = y_dtype == SPLITQ_F32 ? G2_F32 : y_dtype == SPLITQ_F16 ? G2_F16 : G2_BF16;
@@ -874,7 +903,10 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   g.p.out = y;
   g.p.ldo = y_ld;
   if (raw) g.p.raw_aux = reinterpret_cast<float*>(reinterpret_cast<int*>(y) + T * y_ld);
-  bool ok = map_i8(&g.maps.a, at(W.a_main), T, L->k_nat, L->ld_main, 128);
+  // box rows per CTA: the A slot holds 128 rows, the B slot bn / 2; with
+  // swap-AB the weights take the A slot and the token rows the B slot
+  const uint32_t act_box = sw ? g.p.bn / 2 : 128, w_box = sw ? 128 : g.p.bn / 2;
+  bool ok = map_i8(&g.maps.a, at(W.a_main), T, L->k_nat, L->ld_main, act_box);
   // Packed 4-bit weights pay where the GEMM streams weights (few token rows:
   // decode); for large token counts the kernel is tensor / SMEM-bandwidth
   // bound and the SMEM unpack traffic (+50% over the UMMA operand reads at
@@ -884,19 +916,27 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   if (L->bp_main && !raw_unpacked(flags) && T <= packed_max_rows) {
     g.p.packed_b = 1;
     ok = ok && make_map_2d(&g.maps.b, L->bp_main, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, L->d_out,
-                           L->ld_main / 2, L->ld_main / 2, g.p.bn / 2, 64,
-                           CU_TENSOR_MAP_SWIZZLE_NONE);
+                           L->ld_main / 2, L->ld_main / 2, w_box, 64, CU_TENSOR_MAP_SWIZZLE_NONE);
   } else {
-    ok = ok && map_i8(&g.maps.b, L->b_main, L->d_out, L->k_nat, L->ld_main, g.p.bn / 2);
+    ok = ok && map_i8(&g.maps.b, L->b_main, L->d_out, L->k_nat, L->ld_main, w_box);
   }
   g.maps.xa = g.maps.xb = g.maps.a;
   if (ok && L->k_lr)
-    ok = map_f16(&g.maps.xa, lr_a, T, L->k_lr, L->k_lr, 128) &&
-         map_f16(&g.maps.xb, L->b_lr, L->d_out, L->k_lr, L->k_lr, g.p.bn / 2);
+    ok = map_f16(&g.maps.xa, lr_a, T, L->k_lr, L->k_lr, act_box) &&
+         map_f16(&g.maps.xb, L->b_lr, L->d_out, L->k_lr, L->k_lr, w_box);
   if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (split GEMM)");
   if ((rc = launch_gemm(g, L->device, T, stream, at(W.acc_scratch), W.acc_scratch_bytes))) return rc;
   if (prof && (rc = prof_record(L, stream))) return rc;
   return SPLITQ_OK;
+}
+
+// G2_TRACE builds: copy the phase stamps of the last GEMM launch (host buffer
+// of 148 * 8 u64); returns the number of CTAs. Not part of the public ABI.
+int splitq_debug_gemm_trace(unsigned long long* out) {
+  if (!g2_trace_last) return 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(out, g2_trace_last, 148 * 8 * 8, cudaMemcpyDeviceToHost);
+  return g2_trace_ctas;
 }
 
 int splitq_profile_read(splitq_layer_t L, double* stage_ms, int32_t* calls) {
