@@ -44,7 +44,7 @@
 namespace splitq {
 
 constexpr int G2_BM = 256;                 // rows per CTA pair
-constexpr int G2_BN = 128;                 // max tile N with the aux accumulator
+constexpr int G2_BN = 160;                 // max tile N with the aux accumulator (3 bn <= 512 TMEM cols)
 constexpr int G2_BN_MAX = 256;             // max tile N without it
 constexpr int G2_A_BYTES = 128 * 128;      // per CTA: 128 rows x 128 B
 constexpr int G2_MAX_STAGES = 12;
@@ -250,7 +250,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
   uint64_t* bfull = empty + G2_MAX_STAGES;  // packed staging landed (local)
   uint64_t* tfull = bfull + G2_MAX_STAGES;  // [2]
   uint64_t* tempty = tfull + 2;          // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* aempty = tempty + 2;         // [1] aux accumulator drained by the epilogue
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -261,6 +262,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
   const int n_tiles = ((p.swap ? M : p.N) + p.bn - 1) / p.bn;
   const int num_tiles = m_tiles * n_tiles;
   const int pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
+  // K loop per tile: the n_main int8 chunks first, then the n_aux fp16 chunks.
+  // TMEM: main accumulators double-buffered at columns [0, bn) and [bn, 2bn),
+  // the aux accumulator single-buffered at [2bn, 3bn): it is written only at
+  // the end of a tile's K loop, so the epilogue of tile t drains it while tile
+  // t+1's main chunks run (aempty), and bn can be 160 with the aux branch.
   const int n_aux = p.k_aux / 64, n_main = g2_chunks(p.k_main);
   const int stages_per_tile = n_aux + n_main;
   const int ksplit = p.k_split > 1 ? p.k_split : 1;
@@ -284,6 +290,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
     }
+    mbar_init(aempty, 8);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, G2_TMEM_COLS);
@@ -316,7 +323,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + G2_A_BYTES;
           if (elect_one()) {
-            const bool pk = PACKED && v >= n_aux;
+            const bool pk = PACKED && v < n_main;
             if (leader) mbar_arrive_expect_tx(&full[stage], pk ? tx_a : tx);
             // bfull advances once per ring slot use (packed: with the staging
             // bytes; otherwise a plain arrival) so its phase stays in lockstep
@@ -326,12 +333,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
             const CUtensorMap* bm = p.swap ? &maps.a : &maps.b;
             const CUtensorMap* axm = p.swap ? &maps.xb : &maps.xa;  // aux
             const CUtensorMap* bxm = p.swap ? &maps.xa : &maps.xb;
-            if (v < n_aux) {
-              tma_load_2d_pair(sa, axm, &full[stage], v * 64, m0);
-              tma_load_2d_pair(sb, bxm, &full[stage], v * 64, n0);
+            if (v >= n_main) {
+              const int va = v - n_main;
+              tma_load_2d_pair(sa, axm, &full[stage], va * 64, m0);
+              tma_load_2d_pair(sb, bxm, &full[stage], va * 64, n0);
               if (PACKED) mbar_arrive(&bfull[stage]);
             } else {
-              const int c = v - n_aux;
+              const int c = v;
               if (pk) {
                 // activations through the pair TMA; packed weights to the local staging box
                 if (p.swap) tma_load_2d_pair(sb, &maps.a, &full[stage], c * 128, n0);
@@ -357,19 +365,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
     if (leader && num_tiles > 0) {
       int stage = 0;
       uint32_t phase = 0;
-      int it = 0;
+      int it = 0, aux_uses = 0;
       const uint32_t smem0 = smem_u32(smem);
       for (int item = pair; item < num_items; item += num_pairs, ++it) {
         int tile, s0, s1;
         item_of(item, tile, s0, s1);
-        const int first_main = s0 > n_aux ? s0 : n_aux;  // first main / aux stage of the range
+        const int first_aux = s0 > n_main ? s0 : n_main;  // first aux stage of the range
         const int b = it & 1;
         const uint32_t tph = (it >> 1) & 1;
         mbar_wait(&tempty[b], tph ^ 1);
         tc_fence_after();
-        // with the aux accumulator: [main 128 | aux 128] per buffer; without: main bn
-        const uint32_t d_main = tmem + b * (n_aux ? 256 : p.bn);
-        const uint32_t d_aux = d_main + 128;
+        const uint32_t d_main = tmem + b * p.bn;
+        const uint32_t d_aux = tmem + 2 * p.bn;
         for (int v = s0; v < s1; ++v) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -377,20 +384,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
           const uint32_t a_addr = smem0 + stage * STAGE_BYTES;
           const uint64_t ad = sw128_kmajor_desc(a_addr);
           const uint64_t bd = sw128_kmajor_desc(a_addr + G2_A_BYTES);
-          if (v < n_aux) {
+          if (v >= n_main) {
+            if (v == first_aux) {  // the previous tile's epilogue has drained the aux accumulator
+              if (aux_uses > 0) mbar_wait(aempty, (uint32_t)((aux_uses - 1) & 1));
+              ++aux_uses;
+              tc_fence_after();
+            }
             if (elect_one()) {
 #pragma unroll
               for (int k = 0; k < 4; ++k)  // K = 16 fp16 (32 B) per MMA
-                mma_f16_pair(d_aux, ad + 2 * k, bd + 2 * k, p.idesc_aux, (v != s0) || k != 0);
+                mma_f16_pair(d_aux, ad + 2 * k, bd + 2 * k, p.idesc_aux, (v != first_aux) || k != 0);
               tc_commit_pair(&empty[stage]);
             }
           } else {
-            const int c = v - n_aux;
+            const int c = v;
             const int nk = (p.k_main - c * 128 + 31) / 32;  // K = 32 int8 per MMA
             if (elect_one()) {
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                if (k < nk) mma_i8_pair(d_main, ad + 2 * k, bd + 2 * k, p.idesc_main, (v != first_main) || k != 0);
+                if (k < nk) mma_i8_pair(d_main, ad + 2 * k, bd + 2 * k, p.idesc_main, (v != s0) || k != 0);
               tc_commit_pair(&empty[stage]);
             }
           }
@@ -417,7 +429,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
         item_of(item, tile, s0, s1);
         for (int v = s0; v < s1; ++v) {
           mbar_wait(&empty[stage], phase ^ 1);  // previous use of the slot drained
-          if (v >= n_aux) {
+          if (v < n_main) {
             mbar_wait(&bfull[stage], phase);
             uint8_t* sb = smem + stage * STAGE_BYTES + W_OFF;
             const uint8_t* sp = smem + stage * STAGE_BYTES + STG_OFF;
@@ -446,13 +458,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
     const int lq = warp & 3;                 // TMEM lane quarter
     const int r_local = lq * 32 + lane;
     const uint32_t tempty_leader = mapa_shared(&tempty[0], 0);
+    const uint32_t aempty_leader = mapa_shared(aempty, 0);
     const bool aux_buf = p.k_aux > 0;  // TMEM layout has the aux half
     int it = 0;
     for (int item = pair; item < num_items; item += num_pairs, ++it) {
       int tile, s0, s1;
       item_of(item, tile, s0, s1);
-      const bool has_aux = aux_buf && s0 < n_aux;               // range touched the aux accumulator
-      const bool has_main = s1 > (s0 > n_aux ? s0 : n_aux);     // ... and the main one
+      const bool has_aux = aux_buf && s1 > (s0 > n_main ? s0 : n_main);  // range touched the aux accumulator
+      const bool has_main = s0 < n_main;                                 // ... and the main one
       const int b = it & 1;
       const uint32_t tph = (it >> 1) & 1;
       const int m0 = (tile / n_tiles) * G2_BM + (int)rank * 128;
@@ -464,7 +477,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
         mbar_wait(&tfull[b], tph);
         tc_fence_after();
         if (warp == 2 && lane == 0 && it == 0) G2_STAMP(6);  // accumulator ready
-        const uint32_t lb = tmem + ((uint32_t)(lq * 32) << 16) + b * (aux_buf ? 256 : p.bn);
+        const uint32_t lb = tmem + ((uint32_t)(lq * 32) << 16) + b * p.bn;
+        const uint32_t lba = tmem + ((uint32_t)(lq * 32) << 16) + 2 * p.bn;  // aux accumulator
         // per-channel constants once; per-token ones loaded by lane jj of the
         // chunk and broadcast with shuffles (no per-element global loads)
         const float sw_j = j_ok && p.col_s ? p.col_s[j] : 0.f;
@@ -475,7 +489,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
         for (int c0 = 0; c0 < p.bn; c0 += 32) {
           uint32_t am[32], af[32];
           tmem_ld32(lb + c0, am);
-          if (has_aux) tmem_ld32(lb + 128 + c0, af);
+          if (has_aux) tmem_ld32(lba + c0, af);
           tmem_wait_ld();
           const int il = n0 + c0 + lane;
           const bool il_ok = il < M;
@@ -536,7 +550,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(b * sizeof(uint64_t)));
+        if (lane == 0) {
+          mbar_arrive_cluster(tempty_leader + (uint32_t)(b * sizeof(uint64_t)));
+          if (has_aux) mbar_arrive_cluster(aempty_leader);
+        }
         continue;
       }
       const int row = m0 + r_local;
@@ -551,11 +568,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
         if (p.row_zp) zp = p.row_zp[row];
         if (has_aux && p.row_rho) rho = p.row_rho[row];
       }
-      const uint32_t lane_base = tmem + ((uint32_t)(lq * 32) << 16) + b * (aux_buf ? 256 : p.bn);
+      const uint32_t lane_base = tmem + ((uint32_t)(lq * 32) << 16) + b * p.bn;
+      const uint32_t lane_aux = tmem + ((uint32_t)(lq * 32) << 16) + 2 * p.bn;
       for (int c0 = 0; c0 < p.bn; c0 += 32) {
         uint32_t am[32], af[32];
         tmem_ld32(lane_base + c0, am);
-        if (has_aux) tmem_ld32(lane_base + 128 + c0, af);
+        if (has_aux) tmem_ld32(lane_aux + c0, af);
         tmem_wait_ld();
         if (!row_ok) continue;
         if (p.mode == G2_ACC) {
@@ -659,7 +677,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(b * sizeof(uint64_t)));
+      if (lane == 0) {
+        mbar_arrive_cluster(tempty_leader + (uint32_t)(b * sizeof(uint64_t)));
+        if (has_aux) mbar_arrive_cluster(aempty_leader);
+      }
     }
   }
 

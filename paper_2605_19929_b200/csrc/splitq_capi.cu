@@ -46,6 +46,16 @@ int fail(int code, const char* fmt, ...) {
 
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
+// tile N: up to 160 with the fp32 aux accumulator (two main buffers + one aux
+// buffer = 3 bn TMEM columns), up to 256 without it (two main buffers)
+int tile_n(int64_t n, bool aux) {
+  if (aux) {  // 160-wide tiles unless the last tile would waste > 5 % of the columns
+    const int64_t r160 = round_up(n, G2_BN);
+    if (n > 128 && r160 * 100 > n * 105) return 128;
+  }
+  return (int)std::min<int64_t>(aux ? G2_BN : G2_BN_MAX, round_up(n, 32));
+}
+
 // calls with at most this many token rows run the GEMMs swap-AB (decode)
 constexpr int64_t kSwapMaxRows = 128;
 inline bool use_swap(int64_t T) { return T <= kSwapMaxRows && !getenv("SPLITQ_NO_SWAP"); }
@@ -503,7 +513,7 @@ int splitq_workspace_layout(splitq_layer_t L, int64_t T, splitq_ws_layout_t* o) 
     const int64_t pairs = sm_count(L->device) / 2;
     const int64_t m_tiles = (T + 255) / 256;
     int64_t need = 0;
-    const int64_t bn = std::min<int64_t>(L->k_lr ? 128 : 256, round_up(L->d_out, 32));
+    const int64_t bn = tile_n(L->d_out, L->k_lr > 0);
     const bool swap = T <= kSwapMaxRows;
     const int64_t kmax = 8;  // split-K slices the scratch holds
     if (swap || m_tiles * ((L->d_out + bn - 1) / bn) * 2 <= pairs)
@@ -607,11 +617,8 @@ bool map_f16(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64
                      64);
 }
 
-// tile N: up to 128 with the fp32 aux accumulator (two buffers of main + aux),
-// up to 256 without it (two buffers of main)
-int tile_n(int64_t n, bool aux) {
-  return (int)std::min<int64_t>(aux ? G2_BN : G2_BN_MAX, round_up(n, 32));
-}
+// tile N: up to 160 with the fp32 aux accumulator (two main buffers + one aux
+// buffer = 3 bn TMEM columns), up to 256 without it (two main buffers)
 
 // i8 MMA instruction descriptor for the pair (M = 256), f16 likewise
 uint32_t idesc_i8(bool a_signed, int bn) { return make_idesc(2, a_signed ? 1u : 0u, 1, G2_BM, bn); }
