@@ -193,6 +193,23 @@ __device__ __forceinline__ void kw_load(const K1Params& p, const uint4* xg, int 
   d[4] = db.x; d[5] = db.y; d[6] = db.z; d[7] = db.w;
 }
 
+// the same from the row group's SMEM copy (x plane + two d planes)
+template <typename T>
+__device__ __forceinline__ void kw_load_s(const uint4* xs, const float4* ds, int nch, int j,
+                                          float (&x)[8], float (&d)[8]) {
+  const uint4 w = xs[j];
+  const float4 da = ds[j], db = ds[nch + j];
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const float2 f2 = XW<T>::to_f2(ws[h]);
+    x[2 * h] = f2.x;
+    x[2 * h + 1] = f2.y;
+  }
+  d[0] = da.x; d[1] = da.y; d[2] = da.z; d[3] = da.w;
+  d[4] = db.x; d[5] = db.y; d[6] = db.z; d[7] = db.w;
+}
+
 __device__ __forceinline__ void kw_mulz(const float (&x)[8], const float (&d)[8], float (&z)[8]) {
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
@@ -313,6 +330,32 @@ __device__ __forceinline__ double kw_warp_maxd(double v) {
   return ounkey_d(((unsigned long long)hi << 32) | lo);
 }
 
+// Row groups of WPR > 1 warps (decode-sized calls: one CTA per row): the
+// warp-uniform values of NV order-preserving u64 keys meet in SMEM (one slot
+// block per call site, so consecutive sites need one barrier each); min.
+template <int WPR, int NV>
+__device__ __forceinline__ void kw_gmin(uint64_t* red, uint64_t (&k)[NV]) {
+  if constexpr (WPR > 1) {
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) red[w * NV + v] = k[v];
+    __syncthreads();
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      uint64_t m = red[v];
+      for (int i = 1; i < WPR; ++i) m = min(m, red[i * NV + v]);
+      k[v] = m;
+    }
+  }
+}
+__device__ __forceinline__ uint64_t kw_fkey64(float f) { return (uint64_t)((uint32_t)kw_fkey(f) ^ 0x80000000u); }
+__device__ __forceinline__ float kw_unfkey64(uint64_t k) {
+  const int i = (int)((uint32_t)k ^ 0x80000000u);
+  return __int_as_float(i ^ ((i >> 31) & 0x7FFFFFFF));
+}
+constexpr int KW_RED_SITES = 6;  // SMEM key blocks per row group: sites x WPR x 8 keys
+
 // compute_params (quantizer.py:118-135) returning 1 / S as well
 __device__ __forceinline__ bool kw_params(double lo, double hi, const QSpecDev& s, double* S,
                                           int* zp, double* rS) {
@@ -394,11 +437,11 @@ __device__ __forceinline__ RowParams kw_rowparams(double S, double rS, int zp, i
 // per-lane fp64 extremes of one outlier path (channels lane, lane + 32, ...)
 template <typename T>
 __device__ __forceinline__ void kw_outlier_ext(const T* xrow, const int* cols, const double* d, int n,
-                                               double& lo, double& hi, bool& nan) {
-  const int lane = threadIdx.x & 31;
+                                               double& lo, double& hi, bool& nan, int k0 = -1,
+                                               int step = 32) {
   lo = INFINITY;
   hi = -INFINITY;
-  for (int k = lane; k < n; k += 32) {
+  for (int k = k0 < 0 ? (int)(threadIdx.x & 31) : k0; k < n; k += step) {
     const double z = __dmul_rn((double)kw_x<T>(xrow, __ldg(cols + k)), __ldg(d + k));
     nan |= z != z;
     lo = fmin(lo, z);
@@ -433,30 +476,58 @@ struct KwZ {
 // pass G as 16-bit fixed point (f * 2^15, offset-binary), so pass G does not
 // recompute the row: the extra rounding (<= 2^-16) enters the MAC tie window
 // (kw_consts2 err_extra); rows whose window would get too wide recompute.
-template <typename T, bool SMF>
-__global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d_in) {
+//
+// WPR > 1 (decode-sized calls, few rows): the CTA's WPR warps share one row,
+// chunks strided over all WPR x 32 threads; warp reductions are completed
+// across the group through SMEM (kw_gmin), the per-row parameters are
+// computed redundantly by every warp (deterministic) and stored by warp 0.
+template <typename T, bool SMF, int WPR>
+__global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(const K1Params p, int d_in) {
+  static_assert(!(SMF && WPR > 1), "SMEM MAC fractions are per-warp rows");
   extern __shared__ __align__(16) uint8_t kw_smem[];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5, nwc = blockDim.x >> 5;
+  const int gl = WPR > 1 ? (int)threadIdx.x : lane;  // thread within the row group
+  constexpr int GT = WPR > 1 ? WPR * 32 : 32;          // threads per row group
+  const bool w0 = WPR == 1 || wl == 0;                 // the group's storing warp
   const int nchunks = d_in >> 3;
   uint32_t* q = reinterpret_cast<uint32_t*>(kw_smem) + wl * KW_QCAP;
   uint4* fs = SMF ? reinterpret_cast<uint4*>(kw_smem + nwc * KW_QCAP * 4) + (size_t)wl * nchunks
                   : nullptr;
-  const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  uint64_t* red = reinterpret_cast<uint64_t*>(kw_smem + nwc * KW_QCAP * 4);  // WPR > 1
+  int* s_slot = reinterpret_cast<int*>(red + KW_RED_SITES * WPR * 8);
+  // WPR > 1: the row (x) and its fp32 smoothing factors staged in SMEM by
+  // pass A; the later passes read them there
+  uint4* xs = reinterpret_cast<uint4*>(red + KW_RED_SITES * WPR * 8 + 2);
+  float4* ds = reinterpret_cast<float4*>(xs + nchunks);
+  const int gw = WPR > 1 ? (int)blockIdx.x : (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nw = WPR > 1 ? (int)gridDim.x : (int)((gridDim.x * blockDim.x) >> 5);
   const bool cen = p.act.centered != 0, cena = p.aux.centered != 0;
+  // dependents (the decode GEMVs) may launch now and prefetch their weights
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int row = gw; row < p.T; row += nw) {
+    if constexpr (WPR > 1) __syncthreads();  // the previous row's SMEM reads are done
     const T* xrow = reinterpret_cast<const T*>(p.x) + (int64_t)row * p.ldx;
     const uint4* xg = reinterpret_cast<const uint4*>(xrow);
+    const T* xr = WPR > 1 ? reinterpret_cast<const T*>(xs) : xrow;  // element reads after pass A
+    auto kwl = [&](int j, float (&x)[8], float (&d)[8]) {
+      if constexpr (WPR > 1) kw_load_s<T>(xs, ds, nchunks, j, x, d);
+      else kw_load<T>(p, xg, j, x, d);
+    };
 
     // ------------------------------------------------ pass A: fp32 z and its extremes
     KwExt elo, ehi;  // ehi tracks -max
     kw_ext_init(elo);
     kw_ext_init(ehi);
     uint32_t nm = 0u;
-    for (int j = lane; j < nchunks; j += 32) {
+    for (int j = gl; j < nchunks; j += GT) {
       const uint4 w = kw_ldg(xg + j);
       const float4 da = __ldg(reinterpret_cast<const float4*>(p.d_main32) + 2 * j);
       const float4 db = __ldg(reinterpret_cast<const float4*>(p.d_main32) + 2 * j + 1);
+      if constexpr (WPR > 1) {
+        xs[j] = w;
+        ds[j] = da;
+        ds[nchunks + j] = db;
+      }
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
       const float d[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
       float z[8], nz[8];
@@ -472,9 +543,9 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
       kw_ext_upd(elo, kw_min8(z), j);
       kw_ext_upd(ehi, kw_min8(nz), j);
     }
-    const float L = kw_warp_minf(elo.m1), H = kw_warp_minf(ehi.m1);  // H = -max
+    float L = kw_warp_minf(elo.m1), H = kw_warp_minf(ehi.m1);  // H = -max
     int slot = -1;
-    if (lane == 0) {
+    if (lane == 0 && w0) {
       const uint8_t tg = p.tags ? p.tags[row] : (uint8_t)1;
       if (tg > 1) atomicOr(p.err, ERR_BAD_TAG);
       if (p.use_mac && tg == 0) {
@@ -488,22 +559,44 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     }
     slot = __shfl_sync(0xffffffffu, slot, 0);
 
-    // outlier paths: exact fp64 extremes
+    // outlier paths: exact fp64 extremes (every warp of a group: few channels)
     double tlo, thi, vlo, vhi;
     bool nan = XW<T>::nonfinite(nm);
-    kw_outlier_ext<T>(xrow, p.c_text, p.d_text, p.n_text, tlo, thi, nan);
-    kw_outlier_ext<T>(xrow, p.c_vis, p.d_vis, p.n_vis, vlo, vhi, nan);
-    if (__any_sync(0xffffffffu, nan) || !isfinite(L) || !isfinite(H)) {
-      if (lane == 0) atomicOr(p.err, ERR_NONFINITE);
+    // (a row group spreads the outlier channels over all its threads)
+    kw_outlier_ext<T>(xrow, p.c_text, p.d_text, p.n_text, tlo, thi, nan, WPR > 1 ? gl : -1, GT);
+    kw_outlier_ext<T>(xrow, p.c_vis, p.d_vis, p.n_vis, vlo, vhi, nan, WPR > 1 ? gl : -1, GT);
+    nan = __any_sync(0xffffffffu, nan);
+    if constexpr (WPR > 1) {
+      tlo = kw_warp_mind(tlo);
+      thi = kw_warp_maxd(thi);
+      vlo = kw_warp_mind(vlo);
+      vhi = kw_warp_maxd(vhi);
+      if (lane == 0 && wl == 0) *s_slot = slot;
+      uint64_t k[7] = {kw_fkey64(L), kw_fkey64(H), nan ? 0ull : 1ull, okey_d(tlo), ~okey_d(thi),
+                       okey_d(vlo), ~okey_d(vhi)};
+      kw_gmin<WPR, 7>(red, k);
+      L = kw_unfkey64(k[0]);
+      H = kw_unfkey64(k[1]);
+      nan = k[2] == 0;
+      tlo = ounkey_d(k[3]);
+      thi = ounkey_d(~k[4]);
+      vlo = ounkey_d(k[5]);
+      vhi = ounkey_d(~k[6]);
+      slot = *s_slot;
+    }
+    if (nan || !isfinite(L) || !isfinite(H)) {
+      if (lane == 0 && w0) atomicOr(p.err, ERR_NONFINITE);
       continue;
     }
-    tlo = kw_warp_mind(tlo);
-    thi = kw_warp_maxd(thi);
-    vlo = kw_warp_mind(vlo);
-    vhi = kw_warp_maxd(vhi);
+    if constexpr (WPR == 1) {
+      tlo = kw_warp_mind(tlo);
+      thi = kw_warp_maxd(thi);
+      vlo = kw_warp_mind(vlo);
+      vhi = kw_warp_maxd(vhi);
+    }
     if ((p.n_text > 0 && !(isfinite(tlo) && isfinite(thi))) ||
         (p.n_vis > 0 && !(isfinite(vlo) && isfinite(vhi)))) {
-      if (lane == 0) atomicOr(p.err, ERR_NONFINITE);
+      if (lane == 0 && w0) atomicOr(p.err, ERR_NONFINITE);
       continue;
     }
 
@@ -515,16 +608,16 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     double lo64 = INFINITY, hi64 = -INFINITY;
     if (elo.m1 <= bl || ehi.m1 <= bh) {
       const bool all = elo.m2 <= bl || ehi.m2 <= bh || (elo.m1 <= bl && ehi.m1 <= bh && elo.c1 != ehi.c1);
-      for (int j = all ? lane : (elo.m1 <= bl ? elo.c1 : ehi.c1); j < nchunks; j += 32) {
+      for (int j = all ? gl : (elo.m1 <= bl ? elo.c1 : ehi.c1); j < nchunks; j += GT) {
         float z[8], x[8], d[8];
-        kw_load<T>(p, xg, j, x, d);
+        kwl(j, x, d);
         kw_mulz(x, d, z);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           if (z[u] <= bl || -z[u] <= bh) {
             double z64;
             (void)kw_exact_main;
-            z64 = __dmul_rn((double)kw_x<T>(xrow, 8 * j + u), __ldg(p.d_main + 8 * j + u));
+            z64 = __dmul_rn((double)kw_x<T>(xr, 8 * j + u), __ldg(p.d_main + 8 * j + u));
             if (z[u] <= bl) lo64 = fmin(lo64, z64);
             if (-z[u] <= bh) hi64 = fmax(hi64, z64);
           }
@@ -534,6 +627,12 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     }
     lo64 = kw_warp_mind(lo64);
     hi64 = kw_warp_maxd(hi64);
+    if constexpr (WPR > 1) {
+      uint64_t k[2] = {okey_d(lo64), ~okey_d(hi64)};
+      kw_gmin<WPR, 2>(red + 1 * WPR * 8, k);
+      lo64 = ounkey_d(k[0]);
+      hi64 = ounkey_d(~k[1]);
+    }
 
     // ------------------------------------------------ group parameters, lane-parallel:
     // lane 0 main (act spec), lane 1 text, lane 2 vision (aux spec)
@@ -546,7 +645,7 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
       const double ghi = g_main ? hi64 : g_vis ? vhi : thi;
       const QSpecDev gs = g_main ? p.act : p.aux;
       if (lane < 3 && (lane == 0 || (lane == 1 ? p.n_text : p.n_vis) > 0)) {
-        if (!kw_params(glo, ghi, gs, &gS, &gzp, &grS)) atomicOr(p.err, ERR_SCALE_ZERO);
+        if (!kw_params(glo, ghi, gs, &gS, &gzp, &grS) && w0) atomicOr(p.err, ERR_SCALE_ZERO);
         c = kw_consts2(glo, ghi, gS, grS, gzp, gs, 0.0);
         gsafe = fmax(fabs(glo), fabs(ghi)) * grS < 536870912.0;  // 2^29 (quant_rn range)
       }
@@ -562,7 +661,8 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
                                       __shfl_sync(0xffffffffu, gsafe, 2), p.aux);
     double rho, rrho;
     kw_rho(fmax(S, fmax(p.n_text > 0 ? rt.S : 0.0, p.n_vis > 0 ? rv.S : 0.0)), rho, rrho);
-    if (lane == 0) {
+    if (!w0) {
+    } else if (lane == 0) {
       p.s_main[row] = S;
       if (p.sf_main) p.sf_main[row] = (float)S;
       p.zp_main[row] = zp;
@@ -582,15 +682,15 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     const KwRow r{S, zp};
 
     // ------------------------------------------------ outlier codes + aux segments
-    if (p.n_text > 0)
-      outlier_codes(p, row, xrow, p.c_text, p.d_text, p.n_text, p.ld_text, p.a_text, rt,
+    if (p.n_text > 0 && wl % WPR == 0)
+      outlier_codes(p, row, xr, p.c_text, p.d_text, p.n_text, p.ld_text, p.a_text, rt,
                     rt.S * rrho, p.lr_off_t, p.kt16);
-    if (p.n_vis > 0)
-      outlier_codes(p, row, xrow, p.c_vis, p.d_vis, p.n_vis, p.ld_vis, p.a_vis, rv, rv.S * rrho,
+    if (p.n_vis > 0 && wl % WPR == (WPR > 1 ? 1 : 0))
+      outlier_codes(p, row, xr, p.c_vis, p.d_vis, p.n_vis, p.ld_vis, p.a_vis, rv, rv.S * rrho,
                     p.lr_off_v, p.kv16);
     if (p.k_lr > 0) {  // the low-rank columns of the aux operand row: LR1 fills them
       uint4* lr = reinterpret_cast<uint4*>(p.lr_a + (int64_t)row * p.k_lr + p.lr_off_s);
-      for (int i = lane; i < (p.k_lr - p.lr_off_s) / 8; i += 32) lr[i] = make_uint4(0, 0, 0, 0);
+      for (int i = gl; i < (p.k_lr - p.lr_off_s) / 8; i += GT) lr[i] = make_uint4(0, 0, 0, 0);
     }
 
     // ------------------------------------------------ pass E: main codes (+ f = v - n)
@@ -601,13 +701,13 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     kw_ext_init(fhi);
     int qn = 0;
     if (c.safe) {
-      for (int j0 = 0; j0 < nchunks; j0 += 32) {
-        const int j = j0 + lane;
+      for (int j0 = 0; j0 < nchunks; j0 += GT) {
+        const int j = j0 + gl;
         bool flag = false;
         if (j < nchunks) {
           float z[8], v[8], x[8], d[8];
           uint32_t b[8];
-          kw_load<T>(p, xg, j, x, d);
+          kwl(j, x, d);
           kw_mulz(x, d, z);
           kw_vt(z, c, v, b);
           *reinterpret_cast<uint2*>(arow + 8 * j) = kw_pack_shift(b, c.F);
@@ -643,15 +743,20 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     // exact fallback: the flagged chunks (queue), or every chunk (unsafe row /
     // queue overflow), elements spread over the lanes. MAC: the exact residual
     // of every element of these chunks joins the extreme candidates.
-    const bool allx = !c.safe || qn > KW_QCAP;
+    bool allx = !c.safe || qn > KW_QCAP;
+    if constexpr (WPR > 1) {  // any warp's queue overflow: the whole row runs exactly
+      uint64_t k[1] = {allx ? 0ull : 1ull};
+      kw_gmin<WPR, 1>(red + 2 * WPR * 8, k);
+      allx = k[0] == 0;
+    }
     const int qnE = allx ? 0 : qn;
     const int nfix = 8 * (allx ? nchunks : qn);
     __syncwarp();
     double xlo = INFINITY, xhi = -INFINITY;
-    for (int i = lane; i < nfix; i += 32) {
+    for (int i = allx ? gl : lane; i < nfix; i += allx ? GT : 32) {
       const int ch = 8 * (allx ? i >> 3 : (int)q[i >> 3]) + (i & 7);
       double z64;
-      const int qc = kw_exact_main(p, kw_x<T>(xrow, ch), ch, r, z64);
+      const int qc = kw_exact_main(p, kw_x<T>(xr, ch), ch, r, z64);
       arow[ch] = (int8_t)(cen ? qc - zp : qc);
       if (mac) {
         const double e64 = __dsub_rn(z64, __dmul_rn((double)(qc - zp), S));
@@ -662,7 +767,13 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     if (!mac) continue;
 
     // ------------------------------------------------ MAC: exact residual extremes
-    const float FL = kw_warp_minf(flo.m1), FH = kw_warp_minf(fhi.m1);
+    float FL = kw_warp_minf(flo.m1), FH = kw_warp_minf(fhi.m1);
+    if constexpr (WPR > 1) {
+      uint64_t k[2] = {kw_fkey64(FL), kw_fkey64(FH)};
+      kw_gmin<WPR, 2>(red + 3 * WPR * 8, k);
+      FL = kw_unfkey64(k[0]);
+      FH = kw_unfkey64(k[1]);
+    }
     // |f - e / S| <= vmax 2^-22 (+ the fp32 rounding of f): an absolute band
     const float vmaxf = fmaxf(fabsf(L), fabsf(H)) * c.rs * 1.0001f + 1.0f;
     const float fband = 2.0f * vmaxf * KW_BAND + 1e-12f;
@@ -670,17 +781,17 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     double elo64 = xlo, ehi64 = xhi;
     if (!allx && (flo.m1 <= bfl || fhi.m1 <= bfh)) {
       const bool all = flo.m2 <= bfl || fhi.m2 <= bfh || (flo.m1 <= bfl && fhi.m1 <= bfh && flo.c1 != fhi.c1);
-      for (int j = all ? lane : (flo.m1 <= bfl ? flo.c1 : fhi.c1); j < nchunks; j += 32) {
+      for (int j = all ? gl : (flo.m1 <= bfl ? flo.c1 : fhi.c1); j < nchunks; j += GT) {
         float f[8], x[8], d[8], z[8], v[8];
         uint32_t b[8];
-        kw_load<T>(p, xg, j, x, d);
+        kwl(j, x, d);
         kw_mulz(x, d, z);
         kw_vt(z, c, v, b);
         kw_frac(v, b, c, f);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           if (f[u] <= bfl || -f[u] <= bfh) {
-            const double e64 = kw_exact_e(p, kw_x<T>(xrow, 8 * j + u), 8 * j + u, r);
+            const double e64 = kw_exact_e(p, kw_x<T>(xr, 8 * j + u), 8 * j + u, r);
             if (f[u] <= bfl) elo64 = fmin(elo64, e64);
             if (-f[u] <= bfh) ehi64 = fmax(ehi64, e64);
           }
@@ -690,6 +801,12 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     }
     elo64 = kw_warp_mind(elo64);
     ehi64 = kw_warp_maxd(ehi64);
+    if constexpr (WPR > 1) {
+      uint64_t k[2] = {okey_d(elo64), ~okey_d(ehi64)};
+      kw_gmin<WPR, 2>(red + 4 * WPR * 8, k);
+      elo64 = ounkey_d(k[0]);
+      ehi64 = ounkey_d(~k[1]);
+    }
     KwConsts ce{};
     double Se = 1.0;
     int zpe = 0;
@@ -697,7 +814,7 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     int use_smf = 0;
     if (lane == 0) {
       double rSe;
-      if (!kw_params(elo64, ehi64, p.aux, &Se, &zpe, &rSe)) atomicOr(p.err, ERR_SCALE_ZERO);
+      if (!kw_params(elo64, ehi64, p.aux, &Se, &zpe, &rSe) && w0) atomicOr(p.err, ERR_SCALE_ZERO);
       // f carries |err| <= vmax 2^-22 in units of S (+ 2^-16 when read back from
       // the 16-bit SMEM copy): times S / Se in units of e / Se
       const double ef = (double)vmaxf * 2.384185791015625e-07;
@@ -706,9 +823,11 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
         use_smf = ce.safe && ce.W2 <= 16;
       }
       if (!use_smf) ce = kw_consts2(elo64, ehi64, Se, rSe, zpe, p.aux, ef * (S * rSe) * 1.01);
-      p.s_mac[slot] = Se;
-      p.zp_mac[slot] = zpe;
-      p.lrs_mac[slot] = (float)(Se * rrho);
+      if (w0) {
+        p.s_mac[slot] = Se;
+        p.zp_mac[slot] = zpe;
+        p.lrs_mac[slot] = (float)(Se * rrho);
+      }
       ratio = (float)(S * rSe);
     }
     ce = kw_shfl(ce, 0);
@@ -722,8 +841,8 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
     qn = qnE;  // the chunks flagged in pass E are exact-coded here as well
     const bool allg = allx || !ce.safe;
     if (!allg) {
-      for (int j0 = 0; j0 < nchunks; j0 += 32) {
-        const int j = j0 + lane;
+      for (int j0 = 0; j0 < nchunks; j0 += GT) {
+        const int j = j0 + gl;
         bool flag = false;
         if (j < nchunks) {
           uint32_t be[8];
@@ -744,7 +863,7 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
           } else {
             float f[8], x[8], d[8], z[8], v[8];
             uint32_t b[8];
-            kw_load<T>(p, xg, j, x, d);
+            kwl(j, x, d);
             kw_mulz(x, d, z);
             kw_vt(z, c, v, b);
             kw_frac(v, b, c, f);
@@ -763,12 +882,17 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
         kw_enqueue(q, qn, flag, j);
       }
     }
-    const bool allg2 = allg || qn > KW_QCAP;
+    bool allg2 = allg || qn > KW_QCAP;
+    if constexpr (WPR > 1) {
+      uint64_t k[1] = {allg2 ? 0ull : 1ull};
+      kw_gmin<WPR, 1>(red + 5 * WPR * 8, k);
+      allg2 = k[0] == 0;
+    }
     const int ngix = 8 * (allg2 ? nchunks : qn);
     __syncwarp();
-    for (int i = lane; i < ngix; i += 32) {
+    for (int i = allg2 ? gl : lane; i < ngix; i += allg2 ? GT : 32) {
       const int ch = 8 * (allg2 ? i >> 3 : (int)q[i >> 3]) + (i & 7);
-      const double e64 = kw_exact_e(p, kw_x<T>(xrow, ch), ch, r);
+      const double e64 = kw_exact_e(p, kw_x<T>(xr, ch), ch, r);
       const int qe = kw_exact_code(e64, Se, zpe, p.aux.qmin, p.aux.qmax);
       erow[ch] = (int8_t)(cena ? qe - zpe : qe);
     }
@@ -776,8 +900,9 @@ __global__ void __launch_bounds__(KW_THREADS) k1w_kernel(const K1Params p, int d
   }
 }
 
-inline size_t k1w_smem(int d_in, int warps, bool smf) {
-  return (size_t)warps * (KW_QCAP * 4 + (smf ? (size_t)d_in * 2 : 0));
+inline size_t k1w_smem(int d_in, int warps, bool smf, int wpr = 1) {
+  return (size_t)warps * (KW_QCAP * 4 + (smf ? (size_t)d_in * 2 : 0)) +
+         (wpr > 1 ? (size_t)KW_RED_SITES * wpr * 8 * 8 + 16 + (size_t)d_in * 6 : 0);
 }
 
 }  // namespace splitq

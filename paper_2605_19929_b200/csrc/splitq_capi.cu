@@ -19,6 +19,7 @@
 #include "quantize.cuh"
 #include "quantize_fast.cuh"
 #include "k1w.cuh"
+#include "gemv_decode.cuh"
 #include "tma_host.cuh"
 
 using namespace splitq;
@@ -340,7 +341,10 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
   if ((rc = pack_weight(L, d->q_main, d->s_main, d->n_main, N, L->ld_main, &L->b_main, &L->s_main,
                         &L->cs_main, 1.0, nullptr, d->c_main)))
     return cleanup(rc);
-  if (wsp.qmax - wsp.qmin <= 15 && !getenv("SPLITQ_UNPACKED_W")) {
+  // centred codes must also fit signed 4 bits; packed rows are 16-byte multiples
+  bool fits4 = wsp.qmax - wsp.qmin <= 15 && L->ld_main % 32 == 0;
+  for (int64_t i = 0; fits4 && i < d->n_main * N; ++i) fits4 = d->q_main[i] >= -8 && d->q_main[i] <= 7;
+  if (fits4 && !getenv("SPLITQ_UNPACKED_W")) {
     // W <= 4 bits: the main GEMM streams 4-bit codes (two per byte; byte i of
     // each 32-bit word holds codes 8g+i and 8g+4+i), unpacked in SMEM
     std::vector<uint8_t> bp((size_t)N * (L->ld_main / 2), 0);
@@ -463,6 +467,11 @@ int splitq_layer_destroy(splitq_layer_t L) {
   return SPLITQ_OK;
 }
 
+// LR1 split-K scratch of the decode GEMV: int32 [8 x r_s], [8 x r_c] + counters
+static int64_t gv_scratch_bytes(const splitq_layer_s* L) {
+  return 4 * (8 * (L->r_s + L->r_c) + (L->r_s + 15) / 16 + (L->r_c + 15) / 16);
+}
+
 int splitq_workspace_layout(splitq_layer_t L, int64_t T, splitq_ws_layout_t* o) {
   if (!L || !o) return fail(SPLITQ_ERR_INVALID, "null argument");
   if (T <= 0) return fail(SPLITQ_ERR_INVALID, "batch must contain at least one token");
@@ -473,8 +482,10 @@ int splitq_workspace_layout(splitq_layer_t L, int64_t T, splitq_ws_layout_t* o) 
     off = round_up(off + bytes, 256);
     return at;
   };
-  o->status = take(16);
-  o->n_text = take(16);
+  // status word, MAC row count and (decode GEMV) the LR1 split-K partials +
+  // arrival counters: one contiguous block zeroed by one memset per forward
+  o->status = take(32 + gv_scratch_bytes(L));
+  o->n_text = o->status + 16;
   o->text_idx = take(4 * T);
   o->text_rows = take(4 * T);
   o->ld_main = L->ld_main;
@@ -605,6 +616,94 @@ int launch_gemm(GemmLaunch& g, int device, int64_t max_rows, cudaStream_t stream
   return SPLITQ_OK;
 }
 
+// Decode-sized calls (T <= gemv_max_rows()): CUDA-core GEMV kernels
+// (gemv_decode.cuh) instead of the tensor-core tiles. SPLITQ_GEMV_MAX_ROWS
+// overrides the threshold (0 disables).
+int gemv_max_rows() {
+  static const int v = getenv("SPLITQ_GEMV_MAX_ROWS") ? atoi(getenv("SPLITQ_GEMV_MAX_ROWS")) : GV_MAX_ROWS;
+  return std::min(v, GV_MAX_ROWS);
+}
+
+constexpr int kGvSmemBudget = 216 * 1024;  // dynamic; + 8 KB static partials
+
+// GEMV launch shape from the weight row bytes and the aux K; false when the
+// staged rows leave no room for a 2-deep ring
+bool gv_shape(bool packed, int64_t row_bytes, int k_aux, GvArgs* g, int* smem) {
+  g->nbox = (int)((row_bytes + 127) / 128);
+  g->nbox_aux = k_aux / 64;
+  g->units_main = (g->nbox + GV_BPU - 1) / GV_BPU;
+  g->units_aux = (g->nbox_aux + GV_BPU - 1) / GV_BPU;
+  g->act_stride = packed ? g->nbox * 256 + 16 : g->nbox * 128 + 64;
+  g->aux_stride = k_aux ? g->nbox_aux * 128 + 64 : 0;
+  const int fixed = gv_smem_bytes(g->act_stride, g->aux_stride, 0);
+  g->stages = std::min(GV_MAX_STAGES, (kGvSmemBudget - fixed) / (GV_BPU * GV_BOX_BYTES));
+  *smem = gv_smem_bytes(g->act_stride, g->aux_stride, g->stages);
+  return g->stages >= 2;
+}
+
+template <bool PACKED, bool ASIGNED, bool LR1>
+int launch_gv_t(const GvMaps& maps, const G2Params& p, const GvArgs& g, int smem, int device, cudaStream_t s) {
+  auto* kern = gv_kernel<PACKED, ASIGNED, LR1>;
+  static bool attr[64] = {};
+  if (device >= 0 && device < 64 && !attr[device]) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kGvSmemBudget));
+    attr[device] = true;
+  }
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, GV_THREADS, smem));
+  if (per_sm < 1) return SPLITQ_ERR_UNSUPPORTED;
+  const int blocks = (p.N + 15) / 16;
+  const int grid = std::min(blocks * g.ksplit, per_sm * sm_count(device));
+  // programmatic dependent launch: the CTAs start (and fill their weight
+  // rings) while the preceding kernel finishes; they wait before reading its
+  // outputs. SPLITQ_NO_PDL=1 launches plainly.
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(GV_THREADS);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = getenv("SPLITQ_NO_PDL") ? 0 : 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps, p, g, blocks));
+  return SPLITQ_OK;
+}
+
+// whether a GEMV launch's staged rows and a 2-deep weight ring fit one CTA
+bool gv_fits(bool packed, int64_t row_bytes, int k_aux) {
+  GvArgs g{};
+  int smem;
+  return gv_shape(packed, row_bytes, k_aux, &g, &smem);
+}
+
+// weights: [N x row_bytes] (packed 4-bit or int8 codes); aux weights b_lr [N x k_aux] fp16
+int launch_gv(G2Params p, GvArgs g, const void* w, int64_t row_bytes, const __half* xb, bool packed,
+              bool a_signed, bool lr1, int device, cudaStream_t s) {
+  int smem;
+  const int k_aux = lr1 ? 0 : p.k_aux;
+  if (!gv_shape(packed, row_bytes, k_aux, &g, &smem)) return fail(SPLITQ_ERR_UNSUPPORTED, "GEMV shape");
+  // LR1 (few channel blocks, long K): split K over CTAs so ~one CTA per SM streams
+  g.ksplit = 1;
+  if (lr1 && g.red) {
+    const int blocks = (p.N + 15) / 16;
+    g.ksplit = std::max(1, std::min(g.units_main, sm_count(device) / std::max(blocks, 1)));
+  }
+  GvMaps maps;
+  bool ok = make_map_2d(&maps.w, w, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, p.N, row_bytes, row_bytes, 16, 128);
+  maps.x = maps.w;
+  if (ok && k_aux)
+    ok = make_map_2d(&maps.x, xb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, p.N, k_aux, 2 * (int64_t)k_aux, 16, 64);
+  if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (GEMV)");
+  if (lr1) return a_signed ? launch_gv_t<false, true, true>(maps, p, g, smem, device, s)
+                           : launch_gv_t<false, false, true>(maps, p, g, smem, device, s);
+  if (packed) return a_signed ? launch_gv_t<true, true, false>(maps, p, g, smem, device, s)
+                              : launch_gv_t<true, false, false>(maps, p, g, smem, device, s);
+  return a_signed ? launch_gv_t<false, true, false>(maps, p, g, smem, device, s)
+                  : launch_gv_t<false, false, false>(maps, p, g, smem, device, s);
+}
+
 // K-major int8 operand, box of box_rows rows x 128 bytes (128-B swizzle)
 bool map_i8(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld,
             uint32_t box_rows) {
@@ -649,8 +748,9 @@ template <typename T, bool GA>
 int launch_k1_t(const K1Params& k, int d_in, cudaStream_t s) {
   // rows per group of G warps: keep one row's SMEM at most ~1/8 of the CTA budget
   const int row_bytes = d_in * (int)sizeof(T);
-  const int G = row_bytes <= 12 * 1024 ? 1 : row_bytes <= 24 * 1024 ? 2
-              : row_bytes <= 48 * 1024 ? 4 : 8;
+  int G = row_bytes <= 12 * 1024 ? 1 : row_bytes <= 24 * 1024 ? 2
+        : row_bytes <= 48 * 1024 ? 4 : 8;
+  if (getenv("SPLITQ_K1_G")) G = std::max(G, atoi(getenv("SPLITQ_K1_G")));
   if (k1_group_smem(d_in, (int)sizeof(T), G) > 200 * 1024) return SPLITQ_ERR_UNSUPPORTED;
   switch (G) {
     case 1: return launch_k1_g<T, GA, 1>(k, d_in, s);
@@ -672,22 +772,27 @@ int launch_k1_dt(const K1Params& k, int d_in, cudaStream_t s) {
 
 // K1 warp-per-row (fp16 / bf16 rows, d_in % 8 == 0, 16-B aligned rows):
 // fp32 fast path with certified exact fp64 fallback (k1w.cuh).
-template <typename T, bool SMF>
+template <typename T, bool SMF, int WPR>
 int launch_k1w_t(const K1Params& k, int d_in, int device, cudaStream_t stream) {
-  const int threads = KW_THREADS;
-  const size_t smem = k1w_smem(d_in, threads / 32, SMF);
+  const int threads = WPR > 1 ? WPR * 32 : KW_THREADS;
+  const size_t smem = k1w_smem(d_in, threads / 32, SMF, WPR);
   static int attr_dev[64] = {0};
   if (device >= 0 && device < 64 && !attr_dev[device]) {
-    CUDA_TRY(cudaFuncSetAttribute(k1w_kernel<T, SMF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_TRY(cudaFuncSetAttribute(k1w_kernel<T, SMF, WPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   200 * 1024));
     attr_dev[device] = 1;
   }
   int per_sm = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1w_kernel<T, SMF>, threads, smem));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1w_kernel<T, SMF, WPR>, threads, smem));
   if (per_sm < 1) return SPLITQ_ERR_UNSUPPORTED;
-  const int64_t warps = (int64_t)per_sm * sm_count(device) * (threads / 32);
-  const int64_t grid = (std::min<int64_t>(k.T, warps) + threads / 32 - 1) / (threads / 32);
-  k1w_kernel<T, SMF><<<(unsigned)grid, threads, smem, stream>>>(k, d_in);
+  int64_t grid;
+  if (WPR > 1) {  // one row per CTA
+    grid = std::min<int64_t>(k.T, (int64_t)per_sm * sm_count(device));
+  } else {
+    const int64_t warps = (int64_t)per_sm * sm_count(device) * (threads / 32);
+    grid = (std::min<int64_t>(k.T, warps) + threads / 32 - 1) / (threads / 32);
+  }
+  k1w_kernel<T, SMF, WPR><<<(unsigned)grid, threads, smem, stream>>>(k, d_in);
   CUDA_TRY(cudaGetLastError());
   return SPLITQ_OK;
 }
@@ -699,8 +804,14 @@ int launch_k1w(const K1Params& k, int d_in, int device, cudaStream_t stream) {
   // 0.756 vs 0.696 ms on the 7B q-proj input, so the recompute stays default.
   static const char* env = getenv("SPLITQ_K1_SMF");
   const bool smf = k.use_mac && env && env[0] == '1' && d_in <= 8192;
-  return smf ? launch_k1w_t<T, true>(k, d_in, device, stream)
-             : launch_k1w_t<T, false>(k, d_in, device, stream);
+  // Few rows (decode): a row per CTA of 8 warps, so one row's passes are not
+  // one warp's serial latency chain. SPLITQ_K1_WPR=1|8 overrides.
+  const char* wenv = getenv("SPLITQ_K1_WPR");  // read per call: tests switch it
+  const int wpr_env = wenv ? atoi(wenv) : 0;
+  const bool grouped = wpr_env ? wpr_env > 1 : k.T <= 2 * sm_count(device);
+  if (grouped && !smf) return launch_k1w_t<T, false, 8>(k, d_in, device, stream);
+  return smf ? launch_k1w_t<T, true, 1>(k, d_in, device, stream)
+             : launch_k1w_t<T, false, 1>(k, d_in, device, stream);
 }
 
 bool k1v3_eligible(const K1Params& k, int d_in) {
@@ -778,7 +889,12 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
 
   const bool prof = (flags & SPLITQ_FWD_PROFILE) != 0;
   if (prof && (rc = prof_record(L, stream))) return rc;
-  CUDA_TRY(cudaMemsetAsync(err, 0, 16, stream));
+  // decode-sized calls: CUDA-core / warp-MMA GEMV kernels (gemv_decode.cuh)
+  const bool gv_packed = L->bp_main && !raw_unpacked(flags);
+  const bool gv = T <= gemv_max_rows() && gv_fits(gv_packed, gv_packed ? L->ld_main / 2 : L->ld_main, (int)L->k_lr) &&
+                  gv_fits(false, L->ld_main, 0);
+  // status word + MAC row count (+ the GEMV LR1 split-K partials and counters)
+  CUDA_TRY(cudaMemsetAsync(err, 0, 32 + (gv ? gv_scratch_bytes(L) : 0), stream));
 
   K1Params k{};
   k.x = x;
@@ -831,7 +947,6 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   k.err = err;
   if (k1v3_eligible(k, (int)L->d_in) && !getenv("SPLITQ_K1_LEGACY")) {
     // K1w claims the compact MAC rows itself (text_rows[slot] = row, order-free)
-    CUDA_TRY(cudaMemsetAsync(n_text, 0, sizeof(int), stream));
     k.mac_count = n_text;
     k.mac_rows = text_rows;
     k.text_idx = nullptr;
@@ -868,6 +983,17 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
     g.p.lo_off = (int)lo_off;
     g.p.row_map = row_map;
     g.p.err = err;
+    if (gv) {
+      GvArgs a{};
+      a.a = (const int8_t*)a_codes;
+      a.lda = L->ld_main;
+      a.a_bytes = L->ld_main;
+      uint8_t* scr = base + W.status + 32;  // zeroed with the status block
+      const bool mac = row_map != nullptr;
+      a.red = reinterpret_cast<int*>(scr) + (mac ? 8 * L->r_s : 0);
+      a.cnt = reinterpret_cast<unsigned*>(scr) + 8 * (L->r_s + L->r_c) + (mac ? (L->r_s + 15) / 16 : 0);
+      return launch_gv(g.p, a, bu, L->ld_main, nullptr, false, a_signed, true, L->device, stream);
+    }
     // swap-AB: the A slot (128 rows per CTA) takes the weights, B the token rows
     bool ok = map_i8(&g.maps.a, a_codes, T, L->k_nat, L->ld_main, sw ? g.p.bn / 2 : 128) &&
               map_i8(&g.maps.b, bu, r, L->k_nat, L->ld_main, sw ? 128 : g.p.bn / 2);
@@ -910,6 +1036,22 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   g.p.out = y;
   g.p.ldo = y_ld;
   if (raw) g.p.raw_aux = reinterpret_cast<float*>(reinterpret_cast<int*>(y) + T * y_ld);
+  static const long packed_max_rows = getenv("SPLITQ_PACKED_MAX_ROWS")
+                                          ? atol(getenv("SPLITQ_PACKED_MAX_ROWS")) : 2048;
+  if (gv) {
+    GvArgs a{};
+    a.a = (const int8_t*)at(W.a_main);
+    a.lda = L->ld_main;
+    a.a_bytes = L->ld_main;
+    a.xa = lr_a;
+    const bool pk = gv_packed;
+    if ((rc = launch_gv(g.p, a, pk ? (const void*)L->bp_main : (const void*)L->b_main,
+                        pk ? L->ld_main / 2 : L->ld_main, L->b_lr, pk, L->act.centered, false, L->device,
+                        stream)))
+      return rc;
+    if (prof && (rc = prof_record(L, stream))) return rc;
+    return SPLITQ_OK;
+  }
   // box rows per CTA: the A slot holds 128 rows, the B slot bn / 2; with
   // swap-AB the weights take the A slot and the token rows the B slot
   const uint32_t act_box = sw ? g.p.bn / 2 : 128, w_box = sw ? 128 : g.p.bn / 2;
@@ -918,8 +1060,6 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   // decode); for large token counts the kernel is tensor / SMEM-bandwidth
   // bound and the SMEM unpack traffic (+50% over the UMMA operand reads at
   // 256 x 128 tiles) costs more than it saves, so the int8 expansion is used.
-  static const long packed_max_rows = getenv("SPLITQ_PACKED_MAX_ROWS")
-                                          ? atol(getenv("SPLITQ_PACKED_MAX_ROWS")) : 2048;
   if (L->bp_main && !raw_unpacked(flags) && T <= packed_max_rows) {
     g.p.packed_b = 1;
     ok = ok && make_map_2d(&g.maps.b, L->bp_main, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, L->d_out,

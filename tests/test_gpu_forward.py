@@ -170,6 +170,17 @@ CASES = {
     "f64_input": dict(seed=16, T=128, d_in=512, d_out=256, k_t=16, k_v=16, r_s=8, r_c=8,
                       x_dtype=np.float64),
     "tiny_dout": dict(seed=17, T=64, d_in=128, d_out=12, k_t=4, k_v=4, r_s=2, r_c=3),
+    # decode-sized calls (<= 8 rows): the CUDA-core GEMV kernels
+    "decode_t2": dict(seed=18, T=2, d_in=512, d_out=384, k_t=16, k_v=16, r_s=16, r_c=16, n_vision=0),
+    "decode_t5_a8": dict(seed=19, T=5, d_in=640, d_out=256, k_t=32, k_v=32, r_s=10, r_c=15, abits=8,
+                         n_vision=2),
+    "decode_t8_a3w3": dict(seed=20, T=8, d_in=384, d_out=200, k_t=8, k_v=8, r_s=8, r_c=12, abits=3,
+                           wbits=3, n_vision=3),
+    "decode_t7_ld16": dict(seed=21, T=7, d_in=400, d_out=130, k_t=8, k_v=8, r_s=6, r_c=5, n_vision=1),
+    "decode_t3_sym": dict(seed=22, T=3, d_in=512, d_out=256, k_t=16, k_v=16, r_s=8, r_c=8, a_sym=True,
+                          n_vision=1),
+    "decode_t4_k4096": dict(seed=23, T=4, d_in=4096, d_out=256, k_t=64, k_v=64, r_s=24, r_c=24,
+                            n_vision=1),
 }
 
 
@@ -275,7 +286,7 @@ def test_quantize_rows_matches_oracle():
         np.testing.assert_array_equal(p.zero_points, zo)
 
 
-@pytest.mark.parametrize("name", ["c1_small", "a3w3", "a8w4", "k110_down"])
+@pytest.mark.parametrize("name", ["c1_small", "a3w3", "a8w4", "k110_down", "decode_t2", "decode_t4_k4096"])
 def test_packed_weights_match_int8_weights(name):
     """The main GEMM streams 4-bit packed weight codes (unpacked in SMEM);
     its raw int32 accumulators and outputs equal those of the int8 copy."""

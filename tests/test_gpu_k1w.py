@@ -119,6 +119,13 @@ SHAPES = {
 }
 
 
+@pytest.fixture(params=["1", "8"], ids=["warp_rows", "cta_rows"], autouse=True)
+def k1_row_group(request, monkeypatch):
+    """Every case runs with one warp per row (prefill) and with 8-warp row
+    groups (decode-sized calls); the library reads SPLITQ_K1_WPR per call."""
+    monkeypatch.setenv("SPLITQ_K1_WPR", request.param)
+
+
 @pytest.mark.parametrize("dt", DTS, ids=["f16", "bf16"])
 @pytest.mark.parametrize("name", sorted(SHAPES))
 def test_half_input_parity(name, dt):
