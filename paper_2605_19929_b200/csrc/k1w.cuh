@@ -39,6 +39,13 @@
 namespace splitq {
 
 constexpr int KW_THREADS = 128;  // 4 row warps per CTA
+
+#ifdef KW_TRACE  // phase clocks of CTA 0's first row (tools/k1_trace.py)
+#define KW_STAMP(i) \
+  if (p.trace && blockIdx.x == 0 && threadIdx.x == 0 && row == gw) p.trace[i] = clock64();
+#else
+#define KW_STAMP(i)
+#endif
 constexpr float KW_BAND = 4.76837158e-7f;  // 2^-21
 constexpr int KW_QCAP = 128;  // flagged-chunk queue entries per warp
 
@@ -506,6 +513,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(co
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int row = gw; row < p.T; row += nw) {
     if constexpr (WPR > 1) __syncthreads();  // the previous row's SMEM reads are done
+    KW_STAMP(0)
     const T* xrow = reinterpret_cast<const T*>(p.x) + (int64_t)row * p.ldx;
     const uint4* xg = reinterpret_cast<const uint4*>(xrow);
     const T* xr = WPR > 1 ? reinterpret_cast<const T*>(xs) : xrow;  // element reads after pass A
@@ -514,6 +522,14 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(co
       else kw_load<T>(p, xg, j, x, d);
     };
 
+    // row groups: the outlier channel indices and scales of this thread are
+    // fetched before pass A, so only the x gather follows it
+    int pc_t = -1, pc_v = -1;
+    double pd_t = 0.0, pd_v = 0.0;
+    if constexpr (WPR > 1) {
+      if (gl < p.n_text) pc_t = __ldg(p.c_text + gl), pd_t = __ldg(p.d_text + gl);
+      if (gl < p.n_vis) pc_v = __ldg(p.c_vis + gl), pd_v = __ldg(p.d_vis + gl);
+    }
     // ------------------------------------------------ pass A: fp32 z and its extremes
     KwExt elo, ehi;  // ehi tracks -max
     kw_ext_init(elo);
@@ -543,6 +559,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(co
       kw_ext_upd(elo, kw_min8(z), j);
       kw_ext_upd(ehi, kw_min8(nz), j);
     }
+    KW_STAMP(1)
     float L = kw_warp_minf(elo.m1), H = kw_warp_minf(ehi.m1);  // H = -max
     int slot = -1;
     if (lane == 0 && w0) {
@@ -563,8 +580,25 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(co
     double tlo, thi, vlo, vhi;
     bool nan = XW<T>::nonfinite(nm);
     // (a row group spreads the outlier channels over all its threads)
-    kw_outlier_ext<T>(xrow, p.c_text, p.d_text, p.n_text, tlo, thi, nan, WPR > 1 ? gl : -1, GT);
-    kw_outlier_ext<T>(xrow, p.c_vis, p.d_vis, p.n_vis, vlo, vhi, nan, WPR > 1 ? gl : -1, GT);
+    if constexpr (WPR > 1) {
+      kw_outlier_ext<T>(xrow, p.c_text, p.d_text, p.n_text, tlo, thi, nan, gl + GT, GT);
+      kw_outlier_ext<T>(xrow, p.c_vis, p.d_vis, p.n_vis, vlo, vhi, nan, gl + GT, GT);
+      if (pc_t >= 0) {
+        const double z = __dmul_rn((double)kw_x<T>(xrow, pc_t), pd_t);
+        nan |= z != z;
+        tlo = fmin(tlo, z);
+        thi = fmax(thi, z);
+      }
+      if (pc_v >= 0) {
+        const double z = __dmul_rn((double)kw_x<T>(xrow, pc_v), pd_v);
+        nan |= z != z;
+        vlo = fmin(vlo, z);
+        vhi = fmax(vhi, z);
+      }
+    } else {
+      kw_outlier_ext<T>(xrow, p.c_text, p.d_text, p.n_text, tlo, thi, nan);
+      kw_outlier_ext<T>(xrow, p.c_vis, p.d_vis, p.n_vis, vlo, vhi, nan);
+    }
     nan = __any_sync(0xffffffffu, nan);
     if constexpr (WPR > 1) {
       tlo = kw_warp_mind(tlo);
@@ -584,6 +618,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(co
       vhi = ounkey_d(~k[6]);
       slot = *s_slot;
     }
+    KW_STAMP(2)
     if (nan || !isfinite(L) || !isfinite(H)) {
       if (lane == 0 && w0) atomicOr(p.err, ERR_NONFINITE);
       continue;
@@ -634,6 +669,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(co
       hi64 = ounkey_d(~k[1]);
     }
 
+    KW_STAMP(3)
     // ------------------------------------------------ group parameters, lane-parallel:
     // lane 0 main (act spec), lane 1 text, lane 2 vision (aux spec)
     KwConsts c{};
@@ -681,6 +717,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(co
     }
     const KwRow r{S, zp};
 
+    KW_STAMP(4)
     // ------------------------------------------------ outlier codes + aux segments
     if (p.n_text > 0 && wl % WPR == 0)
       outlier_codes(p, row, xr, p.c_text, p.d_text, p.n_text, p.ld_text, p.a_text, rt,
@@ -693,6 +730,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(co
       for (int i = gl; i < (p.k_lr - p.lr_off_s) / 8; i += GT) lr[i] = make_uint4(0, 0, 0, 0);
     }
 
+    KW_STAMP(5)
     // ------------------------------------------------ pass E: main codes (+ f = v - n)
     int8_t* arow = p.a_main + (int64_t)row * p.ld_main;
     const bool mac = slot >= 0;
@@ -743,12 +781,14 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(co
     // exact fallback: the flagged chunks (queue), or every chunk (unsafe row /
     // queue overflow), elements spread over the lanes. MAC: the exact residual
     // of every element of these chunks joins the extreme candidates.
+    KW_STAMP(6)
     bool allx = !c.safe || qn > KW_QCAP;
     if constexpr (WPR > 1) {  // any warp's queue overflow: the whole row runs exactly
       uint64_t k[1] = {allx ? 0ull : 1ull};
       kw_gmin<WPR, 1>(red + 2 * WPR * 8, k);
       allx = k[0] == 0;
     }
+    KW_STAMP(7)
     const int qnE = allx ? 0 : qn;
     const int nfix = 8 * (allx ? nchunks : qn);
     __syncwarp();
@@ -764,6 +804,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(co
         xhi = fmax(xhi, e64);
       }
     }
+    KW_STAMP(8)
     if (!mac) continue;
 
     // ------------------------------------------------ MAC: exact residual extremes
@@ -775,6 +816,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(co
       FH = kw_unfkey64(k[1]);
     }
     // |f - e / S| <= vmax 2^-22 (+ the fp32 rounding of f): an absolute band
+    KW_STAMP(9)
     const float vmaxf = fmaxf(fabsf(L), fabsf(H)) * c.rs * 1.0001f + 1.0f;
     const float fband = 2.0f * vmaxf * KW_BAND + 1e-12f;
     const float bfl = FL + fband, bfh = FH + fband;
@@ -799,6 +841,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(co
         if (!all) break;
       }
     }
+    KW_STAMP(10)
     elo64 = kw_warp_mind(elo64);
     ehi64 = kw_warp_maxd(ehi64);
     if constexpr (WPR > 1) {
@@ -807,6 +850,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(co
       elo64 = ounkey_d(k[0]);
       ehi64 = ounkey_d(~k[1]);
     }
+    KW_STAMP(11)
     KwConsts ce{};
     double Se = 1.0;
     int zpe = 0;
@@ -836,6 +880,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(co
     ratio = __shfl_sync(0xffffffffu, ratio, 0);
     use_smf = __shfl_sync(0xffffffffu, use_smf, 0);
 
+    KW_STAMP(12)
     // ------------------------------------------------ pass G: MAC residual codes
     int8_t* erow = p.a_mac + (int64_t)slot * p.ld_main;
     qn = qnE;  // the chunks flagged in pass E are exact-coded here as well
@@ -882,12 +927,14 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(co
         kw_enqueue(q, qn, flag, j);
       }
     }
+    KW_STAMP(13)
     bool allg2 = allg || qn > KW_QCAP;
     if constexpr (WPR > 1) {
       uint64_t k[1] = {allg2 ? 0ull : 1ull};
       kw_gmin<WPR, 1>(red + 5 * WPR * 8, k);
       allg2 = k[0] == 0;
     }
+    KW_STAMP(14)
     const int ngix = 8 * (allg2 ? nchunks : qn);
     __syncwarp();
     for (int i = allg2 ? gl : lane; i < ngix; i += allg2 ? GT : 32) {
@@ -897,6 +944,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(co
       erow[ch] = (int8_t)(cena ? qe - zpe : qe);
     }
     __syncwarp();
+    KW_STAMP(15)
   }
 }
 

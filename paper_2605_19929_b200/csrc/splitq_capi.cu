@@ -772,6 +772,8 @@ int launch_k1_dt(const K1Params& k, int d_in, cudaStream_t s) {
 
 // K1 warp-per-row (fp16 / bf16 rows, d_in % 8 == 0, 16-B aligned rows):
 // fp32 fast path with certified exact fp64 fallback (k1w.cuh).
+unsigned long long* k1w_trace_last = nullptr;
+
 template <typename T, bool SMF, int WPR>
 int launch_k1w_t(const K1Params& k, int d_in, int device, cudaStream_t stream) {
   const int threads = WPR > 1 ? WPR * 32 : KW_THREADS;
@@ -792,7 +794,17 @@ int launch_k1w_t(const K1Params& k, int d_in, int device, cudaStream_t stream) {
     const int64_t warps = (int64_t)per_sm * sm_count(device) * (threads / 32);
     grid = (std::min<int64_t>(k.T, warps) + threads / 32 - 1) / (threads / 32);
   }
+#ifdef KW_TRACE
+  static unsigned long long* kw_trace_buf = nullptr;
+  if (!kw_trace_buf) cudaMalloc(&kw_trace_buf, 16 * 8);
+  cudaMemsetAsync(kw_trace_buf, 0, 16 * 8, stream);
+  K1Params kt = k;
+  kt.trace = kw_trace_buf;
+  k1w_trace_last = kw_trace_buf;
+  k1w_kernel<T, SMF, WPR><<<(unsigned)grid, threads, smem, stream>>>(kt, d_in);
+#else
   k1w_kernel<T, SMF, WPR><<<(unsigned)grid, threads, smem, stream>>>(k, d_in);
+#endif
   CUDA_TRY(cudaGetLastError());
   return SPLITQ_OK;
 }
@@ -805,11 +817,15 @@ int launch_k1w(const K1Params& k, int d_in, int device, cudaStream_t stream) {
   static const char* env = getenv("SPLITQ_K1_SMF");
   const bool smf = k.use_mac && env && env[0] == '1' && d_in <= 8192;
   // Few rows (decode): a row per CTA of 8 warps, so one row's passes are not
-  // one warp's serial latency chain. SPLITQ_K1_WPR=1|8 overrides.
+  // one warp's serial latency chain (tools/k1_trace.py phase clocks;
+  // 16 warps measured slower: the group barriers cost more than the passes
+  // save). SPLITQ_K1_WPR=1|8|16 overrides.
   const char* wenv = getenv("SPLITQ_K1_WPR");  // read per call: tests switch it
   const int wpr_env = wenv ? atoi(wenv) : 0;
   const bool grouped = wpr_env ? wpr_env > 1 : k.T <= 2 * sm_count(device);
-  if (grouped && !smf) return launch_k1w_t<T, false, 8>(k, d_in, device, stream);
+  if (grouped && !smf)
+    return wpr_env >= 16 ? launch_k1w_t<T, false, 16>(k, d_in, device, stream)  // measured slower
+                         : launch_k1w_t<T, false, 8>(k, d_in, device, stream);
   return smf ? launch_k1w_t<T, true, 1>(k, d_in, device, stream)
              : launch_k1w_t<T, false, 1>(k, d_in, device, stream);
 }
@@ -1079,6 +1095,14 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
 
 // G2_TRACE builds: copy the phase stamps of the last GEMM launch (host buffer
 // of 148 * 8 u64); returns the number of CTAs. Not part of the public ABI.
+// KW_TRACE builds: the 16 phase clocks of the last K1 launch's first row
+int splitq_debug_k1_trace(unsigned long long* out) {
+  if (!k1w_trace_last) return 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(out, k1w_trace_last, 16 * 8, cudaMemcpyDeviceToHost);
+  return 16;
+}
+
 int splitq_debug_gemm_trace(unsigned long long* out) {
   if (!g2_trace_last) return 0;
   cudaDeviceSynchronize();

@@ -119,7 +119,7 @@ SHAPES = {
 }
 
 
-@pytest.fixture(params=["1", "8"], ids=["warp_rows", "cta_rows"], autouse=True)
+@pytest.fixture(params=["1", "8", "16"], ids=["warp_rows", "cta8_rows", "cta16_rows"], autouse=True)
 def k1_row_group(request, monkeypatch):
     """Every case runs with one warp per row (prefill) and with 8-warp row
     groups (decode-sized calls); the library reads SPLITQ_K1_WPR per call."""

@@ -3,7 +3,10 @@
 the seven Qwen2.5-VL-7B decoder projections with packed W4 / W3 weights.
 
 Reports, per batch size and weight width:
-  * the step (seven forwards, replayed as one CUDA graph) in us and tokens/s;
+  * the step (seven forwards, replayed as one CUDA graph) in us and tokens/s,
+    with the forwards in sequence (step_us) and along the decoder block's
+    dataflow, independent projections on parallel streams (step_us_branches:
+    q || k || v, o, gate || up, down);
   * the split-GEMM kernels' time (CUDA events around each launch, stage
     profile) and the HBM bandwidth of their weight streaming:
       algorithmic bytes = packed main codes + 4-bit outlier and
@@ -99,10 +102,55 @@ def main():
             e1.record()
             e1.synchronize()
             step_us = e0.elapsed_time(e1) / a.iters * 1e3
+            # the decoder block's dataflow: q || k || v, o, gate || up, down
+            # (independent projections on their own streams inside one graph;
+            # each projection its own workspace)
+            wss = [torch.empty(int(gl.layout(B).total_bytes), dtype=torch.uint8, device=dev) for _, _, gl in gls]
+            names = [sp.name for _, sp, _ in gls]
+            levels = [["q", "k", "v"], ["o"], ["gate", "up"], ["down"]]
+            streams = [torch.cuda.Stream() for _ in range(3)]
+
+            def step_branches():
+                cur = torch.cuda.current_stream()
+                for lvl in levels:
+                    ev = torch.cuda.Event()
+                    ev.record(cur)
+                    done = []
+                    for j, nm in enumerate(lvl):
+                        i = names.index(nm)
+                        g, sp, gl = gls[i]
+                        st = streams[j]
+                        st.wait_event(ev)
+                        with torch.cuda.stream(st):
+                            gl.run(xs[g], tg, y=ys[i], check=False, ws=wss[i])
+                        e = torch.cuda.Event()
+                        e.record(st)
+                        done.append(e)
+                    for e in done:
+                        cur.wait_event(e)
+
+            graph2 = torch.cuda.CUDAGraph()
+            s2 = torch.cuda.Stream()
+            s2.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s2):
+                step_branches()
+                torch.cuda.synchronize()
+                with torch.cuda.graph(graph2, stream=s2):
+                    step_branches()
+            torch.cuda.synchronize()
+            graph2.replay()
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(a.iters):
+                graph2.replay()
+            e1.record()
+            e1.synchronize()
+            step_br_us = e0.elapsed_time(e1) / a.iters * 1e3
             print(json.dumps({
                 "config": "config4 decode: Qwen2.5-VL-7B q,k,v,o,gate,up,down, all-text tokens",
                 "wbits": wbits, "abits": abits, "batch": B,
                 "step_us": step_us, "tokens_per_s": B / (step_us * 1e-6),
+                "step_us_branches": step_br_us, "tokens_per_s_branches": B / (step_br_us * 1e-6),
                 "gemm_us_total": gemm_total_us, "gemm_us": gemm_us,
                 "weight_bytes_algorithmic": alg_b, "weight_bytes_streamed": str_b,
                 "hbm_gbs_algorithmic": alg_b / (gemm_total_us * 1e-6) / 1e9,

@@ -1,8 +1,7 @@
+# round check: all GPU tests, bench (prefill), decode bench
 set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; rc=$?; echo pytest rc=$rc
+[ $rc -eq 0 ] || exit 1
 timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; echo bench rc=$?
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo ncu1 rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:splitq_gemm -s 20 -c 1 -o gpurun_out/gemm_full python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_gemm.log 2>&1; echo ncu2 rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1_ -s 10 -c 1 -o gpurun_out/k1_full python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_k1.log 2>&1; echo ncu3 rc=$?
+timeout 300 python tools/bench_decode.py --specs 4:4 > gpurun_out/decode_gv.jsonl 2> gpurun_out/decode_gv.err; echo dec rc=$?
