@@ -256,6 +256,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
+  // Programmatic dependent launch: everything up to the first read of a
+  // preceding kernel's output (barrier / TMEM set-up, the first ring slots'
+  // weight loads) overlaps that kernel's tail; the threads that read its
+  // outputs (producer for the activations, epilogue for the row constants)
+  // wait first. A device-side row count is such an output: wait up front.
+  if (p.m_count) asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int M = p.m_count ? *p.m_count : p.M;
   // tile grid: 256-row MMA tiles over tokens (or over output channels, swap)
   const int m_tiles = ((p.swap ? p.N : M) + G2_BM - 1) / G2_BM;
@@ -307,52 +314,77 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
         tma_prefetch(&maps.a);
         tma_prefetch(&maps.b);
       }
-      int stage = 0;
-      uint32_t phase = 0;
       const uint32_t tx = 2u * (G2_A_BYTES + (uint32_t)(p.bn / 2) * 128u);
       // packed main stages: only the activation slot comes through the pair TMA
       const uint32_t tx_a = p.swap ? 2u * (uint32_t)(p.bn / 2) * 128u : 2u * G2_A_BYTES;
       const uint32_t tx_bp = (uint32_t)W_ROWS * 64u;       // local packed staging box
+      // one ring slot's loads; part: 1 = weights (+ the expect_tx), 2 =
+      // activations / aux operand rows, 3 = both. swap-AB: the A slot takes
+      // the weight rows (m0), B the token rows (n0).
+      auto issue = [&](int v, int m0, int n0, int stage, int part) {
+        uint8_t* sa = smem + stage * STAGE_BYTES;
+        uint8_t* sb = sa + G2_A_BYTES;
+        const bool pk = PACKED && v < n_main;
+        if ((part & 1) && leader) mbar_arrive_expect_tx(&full[stage], pk ? tx_a : tx);
+        if (v >= n_main) {
+          const int va = v - n_main;
+          if (part & 1) {
+            if (p.swap) tma_load_2d_pair(sa, &maps.xb, &full[stage], va * 64, m0);
+            else tma_load_2d_pair(sb, &maps.xb, &full[stage], va * 64, n0);
+            if (PACKED) mbar_arrive(&bfull[stage]);
+          }
+          if (part & 2) {
+            if (p.swap) tma_load_2d_pair(sb, &maps.xa, &full[stage], va * 64, n0);
+            else tma_load_2d_pair(sa, &maps.xa, &full[stage], va * 64, m0);
+          }
+        } else if (pk) {
+          // packed weights to the local staging box; activations through the pair TMA.
+          // bfull advances once per ring slot use (packed: with the staging
+          // bytes; otherwise a plain arrival) so its phase stays in lockstep
+          // with the ring phase the unpack warps wait on.
+          if (part & 1) {
+            mbar_arrive_expect_tx(&bfull[stage], tx_bp);
+            tma_load_2d(sa + STG_OFF, &maps.b, &bfull[stage], v * 64, p.swap ? m0 : n0);
+          }
+          if (part & 2) {
+            if (p.swap) tma_load_2d_pair(sb, &maps.a, &full[stage], v * 128, n0);
+            else tma_load_2d_pair(sa, &maps.a, &full[stage], v * 128, m0);
+          }
+        } else {
+          if (part & 1) {
+            if (p.swap) tma_load_2d_pair(sa, &maps.b, &full[stage], v * 128, m0);
+            else tma_load_2d_pair(sb, &maps.b, &full[stage], v * 128, n0);
+            if (PACKED) mbar_arrive(&bfull[stage]);
+          }
+          if (part & 2) {
+            if (p.swap) tma_load_2d_pair(sb, &maps.a, &full[stage], v * 128, n0);
+            else tma_load_2d_pair(sa, &maps.a, &full[stage], v * 128, m0);
+          }
+        }
+      };
+      // the first STAGES ring slots are free: their weight loads go out before
+      // the wait for the preceding kernels, the activation loads after it
+      int pre = 0;
+      for (int item = pair; item < num_items && pre < STAGES; item += num_pairs) {
+        int tile, s0, s1;
+        item_of(item, tile, s0, s1);
+        const int m0 = (tile / n_tiles) * G2_BM + (int)rank * 128;
+        const int n0 = (tile % n_tiles) * p.bn + (int)rank * (p.bn / 2);
+        for (int v = s0; v < s1 && pre < STAGES; ++v, ++pre)
+          if (elect_one()) issue(v, m0, n0, pre, 1);
+      }
+      __syncwarp();
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      int stage = 0, slot = 0;
+      uint32_t phase = 0;
       for (int item = pair; item < num_items; item += num_pairs) {
         int tile, s0, s1;
         item_of(item, tile, s0, s1);
         const int m0 = (tile / n_tiles) * G2_BM + (int)rank * 128;
         const int n0 = (tile % n_tiles) * p.bn + (int)rank * (p.bn / 2);
-        for (int v = s0; v < s1; ++v) {
+        for (int v = s0; v < s1; ++v, ++slot) {
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * STAGE_BYTES;
-          uint8_t* sb = sa + G2_A_BYTES;
-          if (elect_one()) {
-            const bool pk = PACKED && v < n_main;
-            if (leader) mbar_arrive_expect_tx(&full[stage], pk ? tx_a : tx);
-            // bfull advances once per ring slot use (packed: with the staging
-            // bytes; otherwise a plain arrival) so its phase stays in lockstep
-            // with the ring phase the unpack warps wait on.
-            // swap-AB: the A slot takes the weight rows (m0), B the token rows (n0)
-            const CUtensorMap* am = p.swap ? &maps.b : &maps.a;   // A-slot operand, main
-            const CUtensorMap* bm = p.swap ? &maps.a : &maps.b;
-            const CUtensorMap* axm = p.swap ? &maps.xb : &maps.xa;  // aux
-            const CUtensorMap* bxm = p.swap ? &maps.xa : &maps.xb;
-            if (v >= n_main) {
-              const int va = v - n_main;
-              tma_load_2d_pair(sa, axm, &full[stage], va * 64, m0);
-              tma_load_2d_pair(sb, bxm, &full[stage], va * 64, n0);
-              if (PACKED) mbar_arrive(&bfull[stage]);
-            } else {
-              const int c = v;
-              if (pk) {
-                // activations through the pair TMA; packed weights to the local staging box
-                if (p.swap) tma_load_2d_pair(sb, &maps.a, &full[stage], c * 128, n0);
-                else tma_load_2d_pair(sa, &maps.a, &full[stage], c * 128, m0);
-                mbar_arrive_expect_tx(&bfull[stage], tx_bp);
-                tma_load_2d(sa + STG_OFF, &maps.b, &bfull[stage], c * 64, p.swap ? m0 : n0);
-              } else {
-                tma_load_2d_pair(sa, am, &full[stage], c * 128, m0);
-                tma_load_2d_pair(sb, bm, &full[stage], c * 128, n0);
-                if (PACKED) mbar_arrive(&bfull[stage]);
-              }
-            }
-          }
+          if (elect_one()) issue(v, m0, n0, stage, slot < pre ? 2 : 3);
           __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -455,6 +487,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
     }
   } else {
     // ================================================== epilogue (warps 2..5, both CTAs)
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // row constants come from K1
     const int lq = warp & 3;                 // TMEM lane quarter
     const int r_local = lq * 32 + lane;
     const uint32_t tempty_leader = mapa_shared(&tempty[0], 0);
@@ -697,6 +730,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
 // Finalize of a split-K (G2_ACC) launch: one thread per output element;
 // `mode` is the epilogue the single-pass kernel would have run.
 __global__ void g2_finalize_kernel(const G2Params p, int mode, int has_aux) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the split-K slices
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int M = p.m_count ? *p.m_count : p.M;
   const int64_t total = (int64_t)M * p.N;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;

@@ -555,6 +555,12 @@ struct GemmLaunch {
 inline bool raw_unpacked(int flags) { return (flags & SPLITQ_FWD_UNPACKED) != 0; }
 
 unsigned long long* g2_trace_last = nullptr;
+
+// programmatic dependent launch of the GEMM-side kernels (SPLITQ_NO_PDL=1 disables)
+bool pdl_enabled() {
+  static const bool on = !getenv("SPLITQ_NO_PDL");
+  return on;
+}
 int g2_trace_ctas = 0;
 
 int launch_gemm(GemmLaunch& g, int device, int64_t max_rows, cudaStream_t stream,
@@ -601,16 +607,27 @@ int launch_gemm(GemmLaunch& g, int device, int64_t max_rows, cudaStream_t stream
   g2_trace_last = trace_buf;
   g2_trace_ctas = 2 * pairs;
 #endif
-  if (pk)
-    splitq_gemm2_kernel<true><<<2 * pairs, G2_THREADS_PACKED, G2_SMEM_BYTES, stream>>>(g.maps, g.p);
-  else
-    splitq_gemm2_kernel<false><<<2 * pairs, G2_THREADS, G2_SMEM_BYTES, stream>>>(g.maps, g.p);
-  CUDA_TRY(cudaGetLastError());
+  // programmatic dependent launch (set-up and first weight loads overlap the
+  // preceding kernel's tail; see the kernel head)
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cfg.stream = stream;
+  cfg.gridDim = dim3((unsigned)(2 * pairs));
+  cfg.blockDim = dim3(pk ? G2_THREADS_PACKED : G2_THREADS);
+  cfg.dynamicSmemBytes = G2_SMEM_BYTES;
+  if (pk) CUDA_TRY(cudaLaunchKernelEx(&cfg, splitq_gemm2_kernel<true>, g.maps, g.p));
+  else CUDA_TRY(cudaLaunchKernelEx(&cfg, splitq_gemm2_kernel<false>, g.maps, g.p));
   if (g.p.mode == G2_ACC) {
     const int64_t total = max_rows * g.p.N;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4L * sm_count(device));
-    g2_finalize_kernel<<<blocks, 256, 0, stream>>>(g.p, final_mode, has_aux ? 1 : 0);
-    CUDA_TRY(cudaGetLastError());
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, g2_finalize_kernel, g.p, final_mode, has_aux ? 1 : 0));
     g.p.mode = final_mode;
   }
   return SPLITQ_OK;
@@ -664,7 +681,7 @@ int launch_gv_t(const GvMaps& maps, const G2Params& p, const GvArgs& g, int smem
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = getenv("SPLITQ_NO_PDL") ? 0 : 1;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps, p, g, blocks));
