@@ -41,7 +41,7 @@
 
 namespace splitq {
 
-constexpr int GV_MAX_ROWS = 8;
+constexpr int GV_MAX_ROWS = 32;  // NT <= 4 MMA n-tiles of 8 token rows
 constexpr int GV_WARPS = 8;                 // consumer (MMA) warps
 constexpr int GV_THREADS = (GV_WARPS + 1) * 32;  // + one producer (TMA) warp
 constexpr int GV_BPU = 8;         // 128-byte boxes per ring unit (16 KB stages)
@@ -59,8 +59,9 @@ struct GvArgs {
   int act_stride, aux_stride;  // SMEM row strides of the staged activations (bytes)
   const __half* xa;     // aux operand rows [rows x k_aux] (SPLIT / RAW)
   // K split over CTAs (LR1: few channels, long K): ksplit CTAs per channel
-  // block add their int32 partials into red [8 x N] (zeroed by the caller)
-  // and the last to arrive (cnt[block]) applies the epilogue
+  // block add their int32 partials into red [rows x N] (zeroed by the
+  // caller) and the last to arrive (cnt[block * NT + n-tile]) applies the
+  // epilogue
   int ksplit;
   int* red;
   unsigned* cnt;
@@ -71,9 +72,9 @@ struct GvMaps {
   CUtensorMap x;        // aux weights [N x k_aux] (FLOAT16), box 16 x 64
 };
 
-// SMEM: the ring, staged activation rows (8 x act_stride), staged aux rows, barriers
-__host__ __device__ inline int gv_smem_bytes(int act_stride, int aux_stride, int stages) {
-  return 8 * act_stride + 8 * aux_stride + stages * GV_BPU * GV_BOX_BYTES + 2 * GV_MAX_STAGES * 8 + 1024;
+// SMEM: the ring, staged activation rows (rows x act_stride), staged aux rows, barriers
+__host__ __device__ inline int gv_smem_bytes(int rows, int act_stride, int aux_stride, int stages) {
+  return rows * (act_stride + aux_stride) + stages * GV_BPU * GV_BOX_BYTES + 2 * GV_MAX_STAGES * 8 + 1024;
 }
 
 __device__ __forceinline__ uint32_t gv_sext4(uint32_t v) {  // 4 signed nibbles (low) -> 4 int8
@@ -105,9 +106,10 @@ __device__ __forceinline__ void gv_bar_consumers() {  // named barrier of the 8 
   asm volatile("bar.sync 1, %0;" ::"n"(GV_WARPS * 32) : "memory");
 }
 
-template <bool PACKED, bool ASIGNED, bool LR1>
+template <bool PACKED, bool ASIGNED, bool LR1, int NT>
 __global__ void __launch_bounds__(GV_THREADS) gv_kernel(const __grid_constant__ GvMaps maps, const G2Params p,
                                                         const GvArgs g, int blocks) {
+  constexpr int RT = 8 * NT;  // staged token rows
   extern __shared__ __align__(16) uint8_t gv_smem[];
   __shared__ int s_acc[GV_WARPS][32][4];
   __shared__ float s_aux[GV_WARPS][32][4];
@@ -118,8 +120,8 @@ __global__ void __launch_bounds__(GV_THREADS) gv_kernel(const __grid_constant__ 
   // ring first (1024-byte aligned for the 128-byte swizzle), then the rows
   uint8_t* ring = gv_smem + ((1024u - (smem_u32(gv_smem) & 1023u)) & 1023u);
   uint8_t* sact = ring + S * GV_BPU * GV_BOX_BYTES;
-  uint8_t* saux = sact + 8 * g.act_stride;
-  uint64_t* full = reinterpret_cast<uint64_t*>(saux + 8 * g.aux_stride);
+  uint8_t* saux = sact + RT * g.act_stride;
+  uint64_t* full = reinterpret_cast<uint64_t*>(saux + RT * g.aux_stride);
   uint64_t* empty = full + GV_MAX_STAGES;
   // units: main boxes first, then aux boxes; a K split takes a contiguous
   // range of the main units (LR1 only: no aux)
@@ -177,7 +179,7 @@ __global__ void __launch_bounds__(GV_THREADS) gv_kernel(const __grid_constant__ 
   {
     constexpr int PB = PACKED ? 32 : 16;  // activation bytes per weight chunk
     const int pieces = g.nbox * 8;
-    for (int i = threadIdx.x; i < 8 * pieces; i += CT) {
+    for (int i = threadIdx.x; i < RT * pieces; i += CT) {
       const int t = i / pieces, pc = i - t * pieces;
       const int b = pc >> 3, c = pc & 7;
       const int64_t src = (int64_t)(b * 8 + c) * PB;
@@ -193,7 +195,7 @@ __global__ void __launch_bounds__(GV_THREADS) gv_kernel(const __grid_constant__ 
     }
     if (!LR1) {
       const int xp = g.nbox_aux * 8;  // 16-byte pieces
-      for (int i = threadIdx.x; i < 8 * xp; i += CT) {
+      for (int i = threadIdx.x; i < RT * xp; i += CT) {
         const int t = i / max(xp, 1), pc = i - t * xp;
         const int b = pc >> 3, c = pc & 7;
         uint4 v = make_uint4(0, 0, 0, 0);
@@ -202,19 +204,22 @@ __global__ void __launch_bounds__(GV_THREADS) gv_kernel(const __grid_constant__ 
       }
     }
   }
-  // per-thread token constants: tokens 2 tig, 2 tig + 1 (accumulator columns)
-  float t_s[2] = {0.f, 0.f}, t_rho[2] = {0.f, 0.f};
-  int t_zp[2] = {0, 0}, t_orow[2] = {2 * tig, 2 * tig + 1};
+  // per-thread token constants: tokens 8 j + 2 tig + {0, 1} (accumulator columns)
+  float t_s[NT][2], t_rho[NT][2];
+  int t_zp[NT][2], t_orow[NT][2];
 #pragma unroll
-  for (int e = 0; e < 2; ++e) {
-    const int t = 2 * tig + e;
-    if (t < M) {
-      t_s[e] = p.row_s ? p.row_s[t] : 0.f;
-      t_zp[e] = p.row_zp ? p.row_zp[t] : 0;
-      if (!LR1 && p.k_aux > 0 && p.row_rho) t_rho[e] = p.row_rho[t];
-      if (LR1 && p.row_map) t_orow[e] = p.row_map[t];
+  for (int j = 0; j < NT; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int t = 8 * j + 2 * tig + e;
+      t_s[j][e] = 0.f, t_rho[j][e] = 0.f, t_zp[j][e] = 0, t_orow[j][e] = t;
+      if (t < M) {
+        t_s[j][e] = p.row_s ? p.row_s[t] : 0.f;
+        t_zp[j][e] = p.row_zp ? p.row_zp[t] : 0;
+        if (!LR1 && p.k_aux > 0 && p.row_rho) t_rho[j][e] = p.row_rho[t];
+        if (LR1 && p.row_map) t_orow[j][e] = p.row_map[t];
+      }
     }
-  }
   gv_bar_consumers();  // staged rows visible
 
   const uint8_t* arow = sact + gq * g.act_stride;  // this thread's B-operand token row
@@ -224,8 +229,12 @@ __global__ void __launch_bounds__(GV_THREADS) gv_kernel(const __grid_constant__ 
     const int cb = item / ks_n;
     int u0, u1;
     unit_range(item, u0, u1);
-    int acc[4] = {0, 0, 0, 0};
-    float ax[4] = {0.f, 0.f, 0.f, 0.f};
+    int acc[NT][4];
+    float ax[NT][4];
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[j][e] = 0, ax[j][e] = 0.f;
     for (int u = u0; u < u1; ++u, ++li) {
       const bool aux = u >= g.units_main;
       const int b0 = (aux ? u - g.units_main : u) * GV_BPU;
@@ -241,81 +250,100 @@ __global__ void __launch_bounds__(GV_THREADS) gv_kernel(const __grid_constant__ 
         const uint4 wh = *reinterpret_cast<const uint4*>(bx + (gq + 8) * 128 + ((c ^ gq) << 4));
         const int slot = 4 * half + tig;
         if (!aux && PACKED) {
-          const uint4* ap = reinterpret_cast<const uint4*>(arow + (b0 + b) * 256 + slot * 32);
-          const uint4 x0 = ap[0], x1 = ap[1];
           const uint32_t lo[4] = {wl.x, wl.y, wl.z, wl.w}, hi[4] = {wh.x, wh.y, wh.z, wh.w};
-          const uint32_t av[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+          uint32_t fa[4][4];  // unpacked A fragments, shared by the n-tiles
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            gv_mma_i8<ASIGNED>(acc, gv_sext4(lo[i]), gv_sext4(hi[i]), gv_sext4(lo[i] >> 4), gv_sext4(hi[i] >> 4),
-                               av[2 * i], av[2 * i + 1]);
+            fa[i][0] = gv_sext4(lo[i]), fa[i][1] = gv_sext4(hi[i]), fa[i][2] = gv_sext4(lo[i] >> 4),
+            fa[i][3] = gv_sext4(hi[i] >> 4);
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            const uint4* ap =
+                reinterpret_cast<const uint4*>(arow + 8 * j * g.act_stride + (b0 + b) * 256 + slot * 32);
+            const uint4 x0 = ap[0], x1 = ap[1];
+            const uint32_t av[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              gv_mma_i8<ASIGNED>(acc[j], fa[i][0], fa[i][1], fa[i][2], fa[i][3], av[2 * i], av[2 * i + 1]);
+          }
         } else if (!aux) {
-          const uint4 x0 = *reinterpret_cast<const uint4*>(arow + (b0 + b) * 128 + slot * 16);
-          gv_mma_i8<ASIGNED>(acc, wl.x, wh.x, wl.y, wh.y, x0.x, x0.y);
-          gv_mma_i8<ASIGNED>(acc, wl.z, wh.z, wl.w, wh.w, x0.z, x0.w);
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            const uint4 x0 =
+                *reinterpret_cast<const uint4*>(arow + 8 * j * g.act_stride + (b0 + b) * 128 + slot * 16);
+            gv_mma_i8<ASIGNED>(acc[j], wl.x, wh.x, wl.y, wh.y, x0.x, x0.y);
+            gv_mma_i8<ASIGNED>(acc[j], wl.z, wh.z, wl.w, wh.w, x0.z, x0.w);
+          }
         } else {
-          const uint4 x0 = *reinterpret_cast<const uint4*>(xrow + (b0 + b) * 128 + slot * 16);
-          gv_mma_f16(ax, wl.x, wh.x, wl.y, wh.y, x0.x, x0.y);
-          gv_mma_f16(ax, wl.z, wh.z, wl.w, wh.w, x0.z, x0.w);
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            const uint4 x0 =
+                *reinterpret_cast<const uint4*>(xrow + 8 * j * g.aux_stride + (b0 + b) * 128 + slot * 16);
+            gv_mma_f16(ax[j], wl.x, wh.x, wl.y, wh.y, x0.x, x0.y);
+            gv_mma_f16(ax[j], wl.z, wh.z, wl.w, wh.w, x0.z, x0.w);
+          }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + st_i);  // this warp is done with the stage
     }
-    // ---- the 8 warps' partials, summed in warp order by warp 0
+    // ---- per n-tile: the 8 warps' partials, summed in warp order by warp 0
 #pragma unroll
-    for (int e = 0; e < 4; ++e) s_acc[warp][lane][e] = acc[e], s_aux[warp][lane][e] = ax[e];
-    gv_bar_consumers();
-    if (warp == 0) {
+    for (int j = 0; j < NT; ++j) {
+      if (j) gv_bar_consumers();  // s_acc reused
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s_acc[warp][lane][e] = acc[j][e], s_aux[warp][lane][e] = ax[j][e];
+      gv_bar_consumers();
+      if (warp != 0) continue;
+      int sa[4];
+      float sx[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        int sa = 0;
-        float sx = 0.f;
-        for (int w = 0; w < GV_WARPS; ++w) sa += s_acc[w][lane][e], sx += s_aux[w][lane][e];
-        acc[e] = sa, ax[e] = sx;
+        sa[e] = 0, sx[e] = 0.f;
+        for (int w = 0; w < GV_WARPS; ++w) sa[e] += s_acc[w][lane][e], sx[e] += s_aux[w][lane][e];
       }
       bool last = true;
       if (ks_n > 1) {  // K split over CTAs: integer partials meet in global memory (exact)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int col = cb * 16 + gq + 8 * (e >> 1), t = 2 * tig + (e & 1);
-          if (col < p.N && t < M) atomicAdd(g.red + t * p.N + col, acc[e]);
+          const int col = cb * 16 + gq + 8 * (e >> 1), t = 8 * j + 2 * tig + (e & 1);
+          if (col < p.N && t < M) atomicAdd(g.red + t * p.N + col, sa[e]);
         }
         __threadfence();
         __syncwarp();
-        if (lane == 0) s_last = atomicAdd(g.cnt + cb, 1u) == (unsigned)(ks_n - 1);
+        if (lane == 0) s_last = atomicAdd(g.cnt + cb * NT + j, 1u) == (unsigned)(ks_n - 1);
         __syncwarp();
         last = s_last;
         if (last) {
           __threadfence();
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int col = cb * 16 + gq + 8 * (e >> 1), t = 2 * tig + (e & 1);
-            if (col < p.N && t < M) acc[e] = atomicAdd(g.red + t * p.N + col, 0);
+            const int col = cb * 16 + gq + 8 * (e >> 1), t = 8 * j + 2 * tig + (e & 1);
+            if (col < p.N && t < M) sa[e] = atomicAdd(g.red + t * p.N + col, 0);
           }
         }
       }
-      // ---- epilogue: d[e] = (channel cb*16 + gq + 8 (e >> 1), token 2 tig + (e & 1))
+      // ---- epilogue: (channel cb*16 + gq + 8 (e >> 1), token 8 j + 2 tig + (e & 1))
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int col = cb * 16 + gq + 8 * (e >> 1), tk = e & 1, t = 2 * tig + tk;
+        const int col = cb * 16 + gq + 8 * (e >> 1), tk = e & 1, t = 8 * j + 2 * tig + tk;
         if (!last || col >= p.N || t >= M) continue;
-        const int acc_c = acc[e] - (p.row_zp ? t_zp[tk] * p.col_cs[col] : 0);
+        const int acc_c = sa[e] - (p.row_zp ? t_zp[j][tk] * p.col_cs[col] : 0);
         if (LR1) {
           __half* o = reinterpret_cast<__half*>(p.out);
-          const float v = acc_c == 0 ? 0.f : t_s[tk] * p.col_s[col] * (float)acc_c;
+          const float v = acc_c == 0 ? 0.f : t_s[j][tk] * p.col_s[col] * (float)acc_c;
           if (!(fabsf(v) <= 65504.f) && p.err) atomicOr(p.err, 8 /*ERR_LR_RANGE*/);
           const __half hv = __float2half_rn(v);
-          o[(int64_t)t_orow[tk] * p.ldo + p.col_off + col] = hv;
+          o[(int64_t)t_orow[j][tk] * p.ldo + p.col_off + col] = hv;
           if (p.lo_off)
-            o[(int64_t)t_orow[tk] * p.ldo + p.col_off + p.lo_off + col] = __float2half_rn(v - __half2float(hv));
+            o[(int64_t)t_orow[j][tk] * p.ldo + p.col_off + p.lo_off + col] = __float2half_rn(v - __half2float(hv));
         } else if (p.mode == G2_RAW) {
           const int64_t idx = (int64_t)t * p.ldo + col;
-          reinterpret_cast<int*>(p.out)[idx] = acc[e];
-          if (p.k_aux && p.raw_aux) p.raw_aux[idx] = ax[e];
+          reinterpret_cast<int*>(p.out)[idx] = sa[e];
+          if (p.k_aux && p.raw_aux) p.raw_aux[idx] = sx[e];
         } else {
-          float v = t_s[tk] * p.col_s[col] * (float)acc_c;
-          if (p.k_aux > 0) v = fmaf(t_rho[tk] * p.col_kappa[col], ax[e], v);
+          float v = t_s[j][tk] * p.col_s[col] * (float)acc_c;
+          if (p.k_aux > 0) v = fmaf(t_rho[j][tk] * p.col_kappa[col], sx[e], v);
           g2_store1(p, (int64_t)t * p.ldo + col, v);
         }
       }

@@ -467,9 +467,10 @@ int splitq_layer_destroy(splitq_layer_t L) {
   return SPLITQ_OK;
 }
 
-// LR1 split-K scratch of the decode GEMV: int32 [8 x r_s], [8 x r_c] + counters
+// LR1 split-K scratch of the decode GEMV: int32 [32 x r_s], [32 x r_c] + counters
+// (one per channel block and n-tile)
 static int64_t gv_scratch_bytes(const splitq_layer_s* L) {
-  return 4 * (8 * (L->r_s + L->r_c) + (L->r_s + 15) / 16 + (L->r_c + 15) / 16);
+  return 4 * (GV_MAX_ROWS * (L->r_s + L->r_c) + 4 * ((L->r_s + 15) / 16 + (L->r_c + 15) / 16));
 }
 
 int splitq_workspace_layout(splitq_layer_t L, int64_t T, splitq_ws_layout_t* o) {
@@ -633,34 +634,40 @@ int launch_gemm(GemmLaunch& g, int device, int64_t max_rows, cudaStream_t stream
   return SPLITQ_OK;
 }
 
-// Decode-sized calls (T <= gemv_max_rows()): CUDA-core GEMV kernels
-// (gemv_decode.cuh) instead of the tensor-core tiles. SPLITQ_GEMV_MAX_ROWS
-// overrides the threshold (0 disables).
+// Decode-sized calls (T <= gemv_max_rows()): warp-MMA GEMV kernels
+// (gemv_decode.cuh) instead of the tensor-core tiles. The kernels take up to
+// GV_MAX_ROWS = 32 rows (4 n-tiles), but measured on the 7B projections the
+// tcgen05 swap-AB path is faster from 9 rows on (batch 16: 401 vs 427 us,
+// batch 32: 411 vs 606 us per decode step), so the default cut is 8.
+// SPLITQ_GEMV_MAX_ROWS (read per call; 0 disables) overrides it.
 int gemv_max_rows() {
-  static const int v = getenv("SPLITQ_GEMV_MAX_ROWS") ? atoi(getenv("SPLITQ_GEMV_MAX_ROWS")) : GV_MAX_ROWS;
-  return std::min(v, GV_MAX_ROWS);
+  const char* e = getenv("SPLITQ_GEMV_MAX_ROWS");
+  return std::min(e ? atoi(e) : 8, GV_MAX_ROWS);
 }
 
 constexpr int kGvSmemBudget = 216 * 1024;  // dynamic; + 8 KB static partials
 
-// GEMV launch shape from the weight row bytes and the aux K; false when the
-// staged rows leave no room for a 2-deep ring
-bool gv_shape(bool packed, int64_t row_bytes, int k_aux, GvArgs* g, int* smem) {
+inline int gv_ntiles(int64_t rows) { return rows <= 8 ? 1 : rows <= 16 ? 2 : 4; }
+
+// GEMV launch shape from the token rows, the weight row bytes and the aux K;
+// false when the staged rows leave no room for a 2-deep ring
+bool gv_shape(int64_t rows, bool packed, int64_t row_bytes, int k_aux, GvArgs* g, int* smem) {
+  const int rt = 8 * gv_ntiles(rows);
   g->nbox = (int)((row_bytes + 127) / 128);
   g->nbox_aux = k_aux / 64;
   g->units_main = (g->nbox + GV_BPU - 1) / GV_BPU;
   g->units_aux = (g->nbox_aux + GV_BPU - 1) / GV_BPU;
   g->act_stride = packed ? g->nbox * 256 + 16 : g->nbox * 128 + 64;
   g->aux_stride = k_aux ? g->nbox_aux * 128 + 64 : 0;
-  const int fixed = gv_smem_bytes(g->act_stride, g->aux_stride, 0);
+  const int fixed = gv_smem_bytes(rt, g->act_stride, g->aux_stride, 0);
   g->stages = std::min(GV_MAX_STAGES, (kGvSmemBudget - fixed) / (GV_BPU * GV_BOX_BYTES));
-  *smem = gv_smem_bytes(g->act_stride, g->aux_stride, g->stages);
+  *smem = gv_smem_bytes(rt, g->act_stride, g->aux_stride, g->stages);
   return g->stages >= 2;
 }
 
-template <bool PACKED, bool ASIGNED, bool LR1>
+template <bool PACKED, bool ASIGNED, bool LR1, int NT>
 int launch_gv_t(const GvMaps& maps, const G2Params& p, const GvArgs& g, int smem, int device, cudaStream_t s) {
-  auto* kern = gv_kernel<PACKED, ASIGNED, LR1>;
+  auto* kern = gv_kernel<PACKED, ASIGNED, LR1, NT>;
   static bool attr[64] = {};
   if (device >= 0 && device < 64 && !attr[device]) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kGvSmemBudget));
@@ -688,19 +695,30 @@ int launch_gv_t(const GvMaps& maps, const G2Params& p, const GvArgs& g, int smem
   return SPLITQ_OK;
 }
 
-// whether a GEMV launch's staged rows and a 2-deep weight ring fit one CTA
-bool gv_fits(bool packed, int64_t row_bytes, int k_aux) {
-  GvArgs g{};
-  int smem;
-  return gv_shape(packed, row_bytes, k_aux, &g, &smem);
+template <bool PACKED, bool ASIGNED, bool LR1>
+int launch_gv_n(const GvMaps& maps, const G2Params& p, const GvArgs& g, int smem, int rows, int device,
+                cudaStream_t s) {
+  switch (gv_ntiles(rows)) {
+    case 1: return launch_gv_t<PACKED, ASIGNED, LR1, 1>(maps, p, g, smem, device, s);
+    case 2: return launch_gv_t<PACKED, ASIGNED, LR1, 2>(maps, p, g, smem, device, s);
+    default: return launch_gv_t<PACKED, ASIGNED, LR1, 4>(maps, p, g, smem, device, s);
+  }
 }
 
-// weights: [N x row_bytes] (packed 4-bit or int8 codes); aux weights b_lr [N x k_aux] fp16
-int launch_gv(G2Params p, GvArgs g, const void* w, int64_t row_bytes, const __half* xb, bool packed,
+// whether a GEMV launch's staged rows and a 2-deep weight ring fit one CTA
+bool gv_fits(int64_t rows, bool packed, int64_t row_bytes, int k_aux) {
+  GvArgs g{};
+  int smem;
+  return gv_shape(rows, packed, row_bytes, k_aux, &g, &smem);
+}
+
+// weights: [N x row_bytes] (packed 4-bit or int8 codes); aux weights b_lr [N x k_aux] fp16;
+// rows: the launch's token rows (an upper bound when p.m_count is device-side)
+int launch_gv(G2Params p, GvArgs g, int rows, const void* w, int64_t row_bytes, const __half* xb, bool packed,
               bool a_signed, bool lr1, int device, cudaStream_t s) {
   int smem;
   const int k_aux = lr1 ? 0 : p.k_aux;
-  if (!gv_shape(packed, row_bytes, k_aux, &g, &smem)) return fail(SPLITQ_ERR_UNSUPPORTED, "GEMV shape");
+  if (!gv_shape(rows, packed, row_bytes, k_aux, &g, &smem)) return fail(SPLITQ_ERR_UNSUPPORTED, "GEMV shape");
   // LR1 (few channel blocks, long K): split K over CTAs so ~one CTA per SM streams
   g.ksplit = 1;
   if (lr1 && g.red) {
@@ -713,12 +731,12 @@ int launch_gv(G2Params p, GvArgs g, const void* w, int64_t row_bytes, const __ha
   if (ok && k_aux)
     ok = make_map_2d(&maps.x, xb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, p.N, k_aux, 2 * (int64_t)k_aux, 16, 64);
   if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (GEMV)");
-  if (lr1) return a_signed ? launch_gv_t<false, true, true>(maps, p, g, smem, device, s)
-                           : launch_gv_t<false, false, true>(maps, p, g, smem, device, s);
-  if (packed) return a_signed ? launch_gv_t<true, true, false>(maps, p, g, smem, device, s)
-                              : launch_gv_t<true, false, false>(maps, p, g, smem, device, s);
-  return a_signed ? launch_gv_t<false, true, false>(maps, p, g, smem, device, s)
-                  : launch_gv_t<false, false, false>(maps, p, g, smem, device, s);
+  if (lr1) return a_signed ? launch_gv_n<false, true, true>(maps, p, g, smem, rows, device, s)
+                           : launch_gv_n<false, false, true>(maps, p, g, smem, rows, device, s);
+  if (packed) return a_signed ? launch_gv_n<true, true, false>(maps, p, g, smem, rows, device, s)
+                              : launch_gv_n<true, false, false>(maps, p, g, smem, rows, device, s);
+  return a_signed ? launch_gv_n<false, true, false>(maps, p, g, smem, rows, device, s)
+                  : launch_gv_n<false, false, false>(maps, p, g, smem, rows, device, s);
 }
 
 // K-major int8 operand, box of box_rows rows x 128 bytes (128-B swizzle)
@@ -924,8 +942,9 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   if (prof && (rc = prof_record(L, stream))) return rc;
   // decode-sized calls: CUDA-core / warp-MMA GEMV kernels (gemv_decode.cuh)
   const bool gv_packed = L->bp_main && !raw_unpacked(flags);
-  const bool gv = T <= gemv_max_rows() && gv_fits(gv_packed, gv_packed ? L->ld_main / 2 : L->ld_main, (int)L->k_lr) &&
-                  gv_fits(false, L->ld_main, 0);
+  const bool gv = T <= gemv_max_rows() &&
+                  gv_fits(T, gv_packed, gv_packed ? L->ld_main / 2 : L->ld_main, (int)L->k_lr) &&
+                  gv_fits(T, false, L->ld_main, 0);
   // status word + MAC row count (+ the GEMV LR1 split-K partials and counters)
   CUDA_TRY(cudaMemsetAsync(err, 0, 32 + (gv ? gv_scratch_bytes(L) : 0), stream));
 
@@ -1023,9 +1042,10 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
       a.a_bytes = L->ld_main;
       uint8_t* scr = base + W.status + 32;  // zeroed with the status block
       const bool mac = row_map != nullptr;
-      a.red = reinterpret_cast<int*>(scr) + (mac ? 8 * L->r_s : 0);
-      a.cnt = reinterpret_cast<unsigned*>(scr) + 8 * (L->r_s + L->r_c) + (mac ? (L->r_s + 15) / 16 : 0);
-      return launch_gv(g.p, a, bu, L->ld_main, nullptr, false, a_signed, true, L->device, stream);
+      a.red = reinterpret_cast<int*>(scr) + (mac ? GV_MAX_ROWS * L->r_s : 0);
+      a.cnt = reinterpret_cast<unsigned*>(scr) + GV_MAX_ROWS * (L->r_s + L->r_c) +
+              (mac ? 4 * ((L->r_s + 15) / 16) : 0);
+      return launch_gv(g.p, a, (int)T, bu, L->ld_main, nullptr, false, a_signed, true, L->device, stream);
     }
     // swap-AB: the A slot (128 rows per CTA) takes the weights, B the token rows
     bool ok = map_i8(&g.maps.a, a_codes, T, L->k_nat, L->ld_main, sw ? g.p.bn / 2 : 128) &&
@@ -1078,7 +1098,7 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
     a.a_bytes = L->ld_main;
     a.xa = lr_a;
     const bool pk = gv_packed;
-    if ((rc = launch_gv(g.p, a, pk ? (const void*)L->bp_main : (const void*)L->b_main,
+    if ((rc = launch_gv(g.p, a, (int)T, pk ? (const void*)L->bp_main : (const void*)L->b_main,
                         pk ? L->ld_main / 2 : L->ld_main, L->b_lr, pk, L->act.centered, false, L->device,
                         stream)))
       return rc;

@@ -181,6 +181,12 @@ CASES = {
                           n_vision=1),
     "decode_t4_k4096": dict(seed=23, T=4, d_in=4096, d_out=256, k_t=64, k_v=64, r_s=24, r_c=24,
                             n_vision=1),
+    # 9..32 rows: 2 or 4 MMA n-tiles of 8 rows
+    "decode_t16": dict(seed=24, T=16, d_in=512, d_out=384, k_t=16, k_v=16, r_s=16, r_c=16, n_vision=3),
+    "decode_t27_a8": dict(seed=25, T=27, d_in=640, d_out=200, k_t=32, k_v=32, r_s=10, r_c=15, abits=8,
+                          n_vision=5),
+    "decode_t32_a3w3": dict(seed=26, T=32, d_in=2048, d_out=256, k_t=8, k_v=8, r_s=8, r_c=12, abits=3,
+                            wbits=3, n_vision=0),
 }
 
 
@@ -286,7 +292,8 @@ def test_quantize_rows_matches_oracle():
         np.testing.assert_array_equal(p.zero_points, zo)
 
 
-@pytest.mark.parametrize("name", ["c1_small", "a3w3", "a8w4", "k110_down", "decode_t2", "decode_t4_k4096"])
+@pytest.mark.parametrize("name", ["c1_small", "a3w3", "a8w4", "k110_down", "decode_t2", "decode_t4_k4096",
+                                  "decode_t16", "decode_t27_a8"])
 def test_packed_weights_match_int8_weights(name):
     """The main GEMM streams 4-bit packed weight codes (unpacked in SMEM);
     its raw int32 accumulators and outputs equal those of the int8 copy."""
@@ -305,3 +312,14 @@ def test_packed_weights_match_int8_weights(name):
     ya = g.run(xd, td).cpu().numpy()
     yb = g.run(xd, td, unpacked=True).cpu().numpy()
     np.testing.assert_allclose(ya, yb, rtol=1e-5, atol=1e-5 * np.abs(yb).max())
+
+
+@pytest.mark.parametrize("name", ["decode_t16", "decode_t27_a8", "decode_t32_a3w3"])
+def test_gemv_multi_tile(name, monkeypatch):
+    """9..32-row calls forced onto the GEMV kernels (2 / 4 MMA n-tiles; by
+    default such calls take the tcgen05 swap-AB path): codes, int32
+    accumulators and outputs against the oracle."""
+    monkeypatch.setenv("SPLITQ_GEMV_MAX_ROWS", "32")
+    layer, x, tags = _case(**CASES[name])
+    _check_acc(layer, x, tags)
+    _check_out(layer, x, tags)
