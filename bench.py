@@ -66,6 +66,45 @@ def dist_env():
     return world, rank, local
 
 
+_UNIT_BYTES = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def ncu_gemm_traffic(path=None):
+    """DRAM bytes per split-GEMM launch (dram__bytes_read.sum + write.sum) from
+    the committed `ncu --set full` capture of one bench step (profiles/r01,
+    tools/gpu_profile.sh): the mean over the SPLIT-mode launches (the long
+    ones; the LR1 launches of the same kernel are short). None if absent."""
+    path = path or os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01",
+                                "ncu_gemm_r01.json")
+    try:
+        ks = json.load(open(path))["kernels"]
+    except (OSError, ValueError, KeyError):
+        return None
+
+    def dur(v):
+        t, u = v.get("Duration", "0 us").split()
+        return float(t) * {"us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1.0}.get(u, 1e-6)
+
+    def nbytes(v, m):
+        if m not in v:
+            return None
+        return float(v[m]) * _UNIT_BYTES.get(v.get(m + ".unit", "Gbyte"), 1e9)
+
+    rows = [v for k, v in ks.items() if "gemm" in k]
+    if not rows:
+        return None
+    tmax = max(dur(v) for v in rows)
+    tot = []
+    for v in rows:
+        if dur(v) < 0.5 * tmax:
+            continue
+        r, w = nbytes(v, "dram__bytes_read.sum"), nbytes(v, "dram__bytes_write.sum")
+        if r is not None and w is not None:
+            tot.append(r + w)
+    return {"bytes_per_launch": sum(tot) / len(tot), "launches": len(tot), "source": os.path.relpath(path)} \
+        if tot else None
+
+
 def measured_peaks():
     peaks = {}
     for path in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
@@ -311,7 +350,7 @@ def run_ours(args):
             "frac": achieved_tops / peak_tops,
             "peak_source": peak_src,
             "frac_of_datasheet_4500": achieved_tops / DATASHEET_INT8_TOPS,
-            "traffic": None,
+            "traffic": ncu_gemm_traffic(),
             "algorithmic_ops": "2*T*D_in*D_out per projection (dense-equivalent, SURVEY 8(d))",
         },
         "gpu_launches": launches,

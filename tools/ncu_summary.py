@@ -70,6 +70,7 @@ def full(path, out):
             kernels[key][m] = f'{row[h.index("Metric Value")]} {row[h.index("Metric Unit")]}'.strip()
     r = list(csv.reader(io.StringIO(raw))) or [[]]
     h = r[0]
+    units = r[1] if len(r) > 1 else []
     for row in (r[2:] if "ID" in h else []):
         key = f'{row[h.index("ID")]}:{row[h.index("Kernel Name")].split("(")[0]}'
         for i, name in enumerate(h):
@@ -77,6 +78,8 @@ def full(path, out):
             if base in RAW or any(t in name for t in ("pipe_tensor", "mem_tensor_cycles")):
                 if name.endswith(("pct_of_peak_sustained_elapsed", "pct_of_peak_sustained_active", ".sum")):
                     kernels[key][name] = row[i]
+                    if i < len(units) and units[i]:
+                        kernels[key][name + ".unit"] = units[i]
         stalls = {}
         for i, name in enumerate(h):
             if name.startswith("smsp__average_warps_issue_stalled") and name.endswith("per_issue_active.ratio"):
