@@ -56,6 +56,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-tokens", type=int, default=512)
     ap.add_argument("--out-dtype", default="float16", choices=["float16", "bfloat16", "float32"])
+    ap.add_argument("--schedule", default="branches", choices=["serial", "branches"],
+                    help="serial: the seven projections one after another on one stream; branches: "
+                         "the decoder block's independent projections (q||k||v, o, gate||up, down) on "
+                         "parallel streams, each with its own workspace")
     return ap.parse_args()
 
 
@@ -72,8 +76,9 @@ _UNIT_BYTES = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e1
 def ncu_gemm_traffic(path=None):
     """DRAM bytes per split-GEMM launch (dram__bytes_read.sum + write.sum) from
     the committed `ncu --set full` capture of one bench step (profiles/r01,
-    tools/gpu_profile.sh): the mean over the SPLIT-mode launches (the long
-    ones; the LR1 launches of the same kernel are short). None if absent."""
+    tools/gpu_profile.sh): the mean over the captured SPLIT-mode launches
+    (every third launch of the kernel: LR1 CWS, LR1 MAC, split). None if
+    absent. ncu's raw page reports these in Gbyte."""
     path = path or os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01",
                                 "ncu_gemm_r01.json")
     try:
@@ -81,23 +86,15 @@ def ncu_gemm_traffic(path=None):
     except (OSError, ValueError, KeyError):
         return None
 
-    def dur(v):
-        t, u = v.get("Duration", "0 us").split()
-        return float(t) * {"us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1.0}.get(u, 1e-6)
-
     def nbytes(v, m):
         if m not in v:
             return None
         return float(v[m]) * _UNIT_BYTES.get(v.get(m + ".unit", "Gbyte"), 1e9)
 
-    rows = [v for k, v in ks.items() if "gemm" in k]
-    if not rows:
-        return None
-    tmax = max(dur(v) for v in rows)
+    # capture order per projection: LR1 (CWS), LR1 (MAC), split GEMM
+    rows = [v for k, v in sorted(ks.items(), key=lambda kv: int(kv[0].split(":")[0])) if "gemm" in k]
     tot = []
-    for v in rows:
-        if dur(v) < 0.5 * tmax:
-            continue
+    for v in rows[2::3]:
         r, w = nbytes(v, "dram__bytes_read.sum"), nbytes(v, "dram__bytes_write.sum")
         if r is not None and w is not None:
             tot.append(r + w)
@@ -250,10 +247,38 @@ def run_ours(args):
     out_dt = getattr(torch, args.out_dtype)
     ys = [torch.empty((tokens, sp.d_out), dtype=out_dt, device=dev) for _, sp, _ in packed]
     stream = torch.cuda.current_stream()
+    # branches: the block's independent projections share an input group and
+    # run on parallel streams (K1 of one overlaps the tensor-core GEMM of
+    # another: the GEMM's 194 KB of SMEM per SM leaves room for K1 CTAs)
+    names = [sp.name for _, sp, _ in packed]
+    levels = [[n for n in lv if n in names] for lv in (["q", "k", "v"], ["o"], ["gate", "up"], ["down"])]
+    levels = [lv for lv in levels if lv]
+    width = max(len(lv) for lv in levels)
+    side = [torch.cuda.Stream() for _ in range(width)]
+    wss = [ws] + [torch.empty(ws_bytes, dtype=torch.uint8, device=dev) for _ in range(width - 1)] \
+        if args.schedule == "branches" else [ws]
 
     def step(profile=False):
-        for (g, sp, gl), y in zip(packed, ys):
-            gl.run(xs[g], tags, y=y, check=False, ws=ws, profile=profile)
+        if args.schedule == "serial" or profile:
+            for (g, sp, gl), y in zip(packed, ys):
+                gl.run(xs[g], tags, y=y, check=False, ws=ws, profile=profile)
+            return
+        cur = torch.cuda.current_stream()
+        for lv in levels:
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            done = []
+            for j, nm in enumerate(lv):
+                i = names.index(nm)
+                g, sp, gl = packed[i]
+                side[j].wait_event(ev)
+                with torch.cuda.stream(side[j]):
+                    gl.run(xs[g], tags, y=ys[i], check=False, ws=wss[j])
+                e = torch.cuda.Event()
+                e.record(side[j])
+                done.append(e)
+            for e in done:
+                cur.wait_event(e)
 
     # correctness gate before timing: device error word clear
     step()
@@ -279,11 +304,16 @@ def run_ours(args):
         dist.barrier()
     start.record(stream)
     for _ in range(args.steps):
-        step(profile=True)
+        step()
     end.record(stream)
     end.synchronize()
     ms = start.elapsed_time(end)
     clk = clocks.stop()
+    # stage times (CUDA events around K1 / LR1 / split GEMM): a separate
+    # serial pass of the same K steps, outside the timed region
+    for _ in range(args.steps):
+        step(profile=True)
+    torch.cuda.synchronize()
     if world > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -336,6 +366,8 @@ def run_ours(args):
             "parallelism": f"token-sharded replicas x{world}, one 8x8192-token batch per rank "
                            "(no collective on the path)",
             "out_dtype": args.out_dtype, "abits": args.abits, "wbits": args.wbits,
+            "schedule": (args.schedule + (": q||k||v, o, gate||up, down on parallel streams (own workspaces)"
+                                          if args.schedule == "branches" else ": one stream")),
             "l2": "inputs larger than L2 (each projection input >= 470 MB at N=1)",
         },
         "stage_ms_per_step": {"quantize": stage[0] / args.steps, "lowrank_first_stage": stage[1] / args.steps,
