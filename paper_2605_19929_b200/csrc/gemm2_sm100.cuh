@@ -109,7 +109,26 @@ struct G2Params {
   float* acc_f32;
   int64_t ld_acc;
   int64_t acc_slice;    // elements per slice
+  int tile_gm;          // > 0: tiles walk groups of tile_gm m-tiles, m fastest (L2 reuse of B)
 };
+
+// tile index -> (m-tile, n-tile). Default: row-major (n fastest), so the
+// concurrent CTA pairs share one A row block and stream B. With tile_gm > 0
+// (wide N: B larger than an L2 partition), m runs fastest inside groups of
+// tile_gm m-tiles: the group's A slab stays in L2 and B is streamed once per
+// group instead of being re-fetched for every m-tile.
+__device__ __forceinline__ void g2_tile(const G2Params& p, int tile, int m_tiles, int n_tiles, int& mt, int& nt) {
+  if (p.tile_gm <= 0) {
+    mt = tile / n_tiles;
+    nt = tile - mt * n_tiles;
+    return;
+  }
+  const int gsz = p.tile_gm * n_tiles;
+  const int grp = tile / gsz, r = tile - grp * gsz;
+  const int gm = min(p.tile_gm, m_tiles - grp * p.tile_gm);
+  nt = r / gm;
+  mt = grp * p.tile_gm + (r - nt * gm);
+}
 
 // ---------------------------------------------------------------- epilogue math
 // One output of the SPLIT epilogue: y = S_a S_w (acc - zp cs) + rho kappa aux
@@ -368,8 +387,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
       for (int item = pair; item < num_items && pre < STAGES; item += num_pairs) {
         int tile, s0, s1;
         item_of(item, tile, s0, s1);
-        const int m0 = (tile / n_tiles) * G2_BM + (int)rank * 128;
-        const int n0 = (tile % n_tiles) * p.bn + (int)rank * (p.bn / 2);
+        int mt, nt;
+        g2_tile(p, tile, m_tiles, n_tiles, mt, nt);
+        const int m0 = mt * G2_BM + (int)rank * 128;
+        const int n0 = nt * p.bn + (int)rank * (p.bn / 2);
         for (int v = s0; v < s1 && pre < STAGES; ++v, ++pre)
           if (elect_one()) issue(v, m0, n0, pre, 1);
       }
@@ -380,8 +401,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
       for (int item = pair; item < num_items; item += num_pairs) {
         int tile, s0, s1;
         item_of(item, tile, s0, s1);
-        const int m0 = (tile / n_tiles) * G2_BM + (int)rank * 128;
-        const int n0 = (tile % n_tiles) * p.bn + (int)rank * (p.bn / 2);
+        int mt, nt;
+        g2_tile(p, tile, m_tiles, n_tiles, mt, nt);
+        const int m0 = mt * G2_BM + (int)rank * 128;
+        const int n0 = nt * p.bn + (int)rank * (p.bn / 2);
         for (int v = s0; v < s1; ++v, ++slot) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (elect_one()) issue(v, m0, n0, stage, slot < pre ? 2 : 3);
@@ -501,8 +524,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
       const bool has_main = s0 < n_main;                                 // ... and the main one
       const int b = it & 1;
       const uint32_t tph = (it >> 1) & 1;
-      const int m0 = (tile / n_tiles) * G2_BM + (int)rank * 128;
-      const int n0 = (tile % n_tiles) * p.bn;
+      int mt, nt;
+      g2_tile(p, tile, m_tiles, n_tiles, mt, nt);
+      const int m0 = mt * G2_BM + (int)rank * 128;
+      const int n0 = nt * p.bn;
       if (p.swap) {
         // ---- swap-AB: TMEM lane = output channel j, column = token i
         const int j = m0 + r_local;

@@ -598,6 +598,16 @@ int launch_gemm(GemmLaunch& g, int device, int64_t max_rows, cudaStream_t stream
       g.p.mode = G2_ACC;
     }
   }
+  // wide N (gate / up: B beyond an L2 partition): m-fastest tile groups
+  // whose A slab is ~32 MB (measured on the 7B gate / up GEMMs: group of 16-32
+  // m-tiles 4.8-4.9 ms, row-major 5.4 ms, 64: 5.2-5.4 ms, 128: 6.0 ms)
+  g.p.tile_gm = 0;
+  if (!g.p.swap && n_tiles >= 64 && m_tiles > 1) {
+    const int64_t slab = (int64_t)G2_BM * (g.p.k_main + 2 * (int64_t)g.p.k_aux);  // A bytes per m-tile
+    int gm = (int)std::max<int64_t>(4, std::min<int64_t>(64, (32LL << 20) / slab));
+    if (getenv("SPLITQ_TILE_GM")) gm = atoi(getenv("SPLITQ_TILE_GM"));
+    g.p.tile_gm = gm;
+  }
   const int64_t items = tiles * g.p.k_split;
   const int pairs = (int)std::min<int64_t>(items, avail);
 #ifdef G2_TRACE

@@ -170,6 +170,8 @@ CASES = {
     "f64_input": dict(seed=16, T=128, d_in=512, d_out=256, k_t=16, k_v=16, r_s=8, r_c=8,
                       x_dtype=np.float64),
     "tiny_dout": dict(seed=17, T=64, d_in=128, d_out=12, k_t=4, k_v=4, r_s=2, r_c=3),
+    # >= 64 n-tiles: m-fastest tile groups (G2Params.tile_gm)
+    "wide_n": dict(seed=27, T=700, d_in=256, d_out=10400, k_t=8, k_v=8, r_s=8, r_c=8),
     # decode-sized calls (<= 8 rows): the CUDA-core GEMV kernels
     "decode_t2": dict(seed=18, T=2, d_in=512, d_out=384, k_t=16, k_v=16, r_s=16, r_c=16, n_vision=0),
     "decode_t5_a8": dict(seed=19, T=5, d_in=640, d_out=256, k_t=32, k_v=32, r_s=10, r_c=15, abits=8,
