@@ -15,6 +15,16 @@ from .layer import (
     forward,
     forward_reference,
 )
+from .layer_io import (
+    TensorFormatError,
+    load_layer,
+    load_layer_packed,
+    load_packed,
+    load_tensor,
+    save_layer,
+    save_packed,
+    save_tensor,
+)
 from .lowrank import LowRankBranch, SvdFactors, build_branch, default_rank, truncated_svd
 from .mocd import ChannelPartition, MocdConfig, select_topk, trivial_partition
 from .quantizer import (

@@ -64,74 +64,112 @@ def _gran(spec):
     return getattr(g, "value", g)
 
 
-class GpuLayer:
-    """A SplitLayer packed on one device: the C handle plus its geometry."""
+_INTS = ("d_in", "d_out", "n_main", "n_text", "n_vision", "act_bits", "act_sym", "weight_bits", "weight_sym",
+         "aux_bits_floor", "use_cws", "use_mac", "r_cws", "r_mac")
+_CODE_SETS = ("main", "text", "vision", "us", "vs", "uc", "vc")
 
-    def __init__(self, layer, dev=None):
+
+def pack_arrays(layer) -> dict:
+    """Everything splitq_layer_create consumes, as host numpy arrays: the
+    partition, the smoothing scales and the weight side of
+    forward_with_cache (layer.py:137-163) -- integer codes and fp64 column
+    scales computed with the reference's own numpy expressions, so they are
+    bit-exact by construction. Also the payload of a packed blob
+    (layer_io.save_packed)."""
+    if _gran(layer.act_spec) != "per_token":
+        raise ValueError("activation spec must be PER_TOKEN on the GPU path")
+    if _gran(layer.weight_spec) == "per_token":
+        raise ValueError("weight spec must be PER_CHANNEL or PER_TENSOR on the GPU path")
+    p = layer.partition
+    d_out = int(np.asarray(layer.w_main).shape[1])
+    act, wsp = _spec_struct(layer.act_spec), _spec_struct(layer.weight_spec)
+    floor = int(layer.aux_bits_floor)
+    w_aux = layer.weight_spec.with_floor(floor)
+    _spec_struct(w_aux)
+    a = {}
+    d_main = np.ascontiguousarray(layer.p_main.scale, dtype=np.float64)
+    a["scale_main"] = d_main
+    a["scale_text"] = (np.ascontiguousarray(layer.p_text.scale, dtype=np.float64) if len(p.c_text)
+                       else np.zeros(0))
+    a["scale_vision"] = (np.ascontiguousarray(layer.p_vision.scale, dtype=np.float64) if len(p.c_vision)
+                         else np.zeros(0))
+    for k in ("c_main", "c_text", "c_vision"):
+        a[k] = np.ascontiguousarray(getattr(p, k), dtype=np.int64)
+    w_prime = np.asarray(layer.w_main, np.float64) / d_main[:, np.newaxis]  # apply_inv_left
+    ints = dict(d_in=int(p.dim), d_out=d_out, n_main=len(p.c_main), n_text=len(p.c_text),
+                n_vision=len(p.c_vision), act_bits=act.bits, act_sym=act.symmetric, weight_bits=wsp.bits,
+                weight_sym=wsp.symmetric, aux_bits_floor=floor, use_cws=int(bool(layer.use_cws)),
+                use_mac=int(bool(layer.use_mac)), r_cws=0, r_mac=0)
+
+    def put(name, m, spec):
+        q, s = weight_codes(m, spec)
+        a["q_" + name] = np.ascontiguousarray(q, dtype=np.int8)
+        a["s_" + name] = np.ascontiguousarray(s, dtype=np.float64)
+
+    if layer.use_cws:
+        br = layer.branch_smooth
+        v_eff = br.effective_v()
+        r_pre = w_prime - br.u_star @ v_eff  # layer.py:144 (same numpy/BLAS call)
+        put("main", r_pre, layer.weight_spec)
+        put("us", br.u_star, w_aux)
+        put("vs", v_eff, w_aux)
+        ints["r_cws"] = int(br.rank)
+    else:
+        put("main", w_prime, layer.weight_spec)
+    if layer.use_mac:
+        br = layer.branch_comp
+        put("uc", br.u_star, w_aux)
+        put("vc", br.effective_v(), w_aux)
+        ints["r_mac"] = int(br.rank)
+    if len(p.c_text):
+        put("text", np.asarray(layer.w_text, np.float64) / a["scale_text"][:, np.newaxis], w_aux)
+    if len(p.c_vision):
+        put("vision", np.asarray(layer.w_vision, np.float64) / a["scale_vision"][:, np.newaxis], w_aux)
+    for k, v in ints.items():
+        a[k] = np.array(v, dtype=np.int64)
+    return a
+
+
+class GpuLayer:
+    """A SplitLayer packed on one device: the C handle plus its geometry.
+    Built from a layer (weight codes computed here) or from the arrays of a
+    packed blob (layer_io.load_packed: no recomputation)."""
+
+    def __init__(self, layer=None, dev=None, arrays=None):
         lib = _lib.load()
         dev = dev or device()
-        if _gran(layer.act_spec) != "per_token":
-            raise ValueError("activation spec must be PER_TOKEN on the GPU path")
-        if _gran(layer.weight_spec) == "per_token":
-            raise ValueError("weight spec must be PER_CHANNEL or PER_TENSOR on the GPU path")
-        p = layer.partition
-        d_out = int(np.asarray(layer.w_main).shape[1])
-        act, wsp = _spec_struct(layer.act_spec), _spec_struct(layer.weight_spec)
-        floor = int(layer.aux_bits_floor)
-        w_aux = layer.weight_spec.with_floor(floor)
-        _spec_struct(w_aux)
+        a = pack_arrays(layer) if arrays is None else arrays
         keep = []
 
-        def arr(a, dt):
-            a = np.ascontiguousarray(np.asarray(a), dtype=dt)
-            keep.append(a)
-            return a
+        def arr(name, dt):
+            if name not in a:
+                return None
+            v = np.ascontiguousarray(a[name], dtype=dt)
+            keep.append(v)
+            return _ptr(v)
 
-        d_main = arr(layer.p_main.scale, np.float64)
-        d_text = arr(layer.p_text.scale, np.float64) if len(p.c_text) else arr(np.zeros(0), np.float64)
-        d_vis = arr(layer.p_vision.scale, np.float64) if len(p.c_vision) else arr(np.zeros(0), np.float64)
-        # weight side of forward_with_cache (layer.py:137-163), once
-        w_main = np.asarray(layer.w_main, np.float64)
-        w_prime = w_main / d_main[:, np.newaxis]  # apply_inv_left (transform.py:106-115)
+        iv = {k: int(a[k]) for k in _INTS}
         desc = _lib.LayerDesc()
-        desc.d_in, desc.d_out = int(p.dim), d_out
-        desc.n_main, desc.n_text, desc.n_vision = len(p.c_main), len(p.c_text), len(p.c_vision)
-        desc.c_main = _ptr(arr(p.c_main, np.int64))
-        desc.c_text = _ptr(arr(p.c_text, np.int64))
-        desc.c_vision = _ptr(arr(p.c_vision, np.int64))
-        desc.scale_main, desc.scale_text, desc.scale_vision = _ptr(d_main), _ptr(d_text), _ptr(d_vis)
-        desc.act, desc.weight, desc.aux_bits_floor = act, wsp, floor
-        desc.use_cws, desc.use_mac = int(bool(layer.use_cws)), int(bool(layer.use_mac))
-
-        def put(name, m, spec):
-            q, s = weight_codes(m, spec)
-            setattr(desc, "q_" + name, _ptr(arr(q, np.int8)))
-            setattr(desc, "s_" + name, _ptr(arr(s, np.float64)))
-
-        if layer.use_cws:
-            br = layer.branch_smooth
-            v_eff = br.effective_v()
-            r_pre = w_prime - br.u_star @ v_eff  # layer.py:144 (same numpy/BLAS call)
-            put("main", r_pre, layer.weight_spec)
-            put("us", br.u_star, w_aux)
-            put("vs", v_eff, w_aux)
-            desc.r_cws = int(br.rank)
-        else:
-            put("main", w_prime, layer.weight_spec)
-        if layer.use_mac:
-            br = layer.branch_comp
-            put("uc", br.u_star, w_aux)
-            put("vc", br.effective_v(), w_aux)
-            desc.r_mac = int(br.rank)
-        if len(p.c_text):
-            put("text", np.asarray(layer.w_text, np.float64) / d_text[:, np.newaxis], w_aux)
-        if len(p.c_vision):
-            put("vision", np.asarray(layer.w_vision, np.float64) / d_vis[:, np.newaxis], w_aux)
+        desc.d_in, desc.d_out = iv["d_in"], iv["d_out"]
+        desc.n_main, desc.n_text, desc.n_vision = iv["n_main"], iv["n_text"], iv["n_vision"]
+        desc.c_main, desc.c_text, desc.c_vision = (arr("c_main", np.int64), arr("c_text", np.int64),
+                                                   arr("c_vision", np.int64))
+        desc.scale_main, desc.scale_text, desc.scale_vision = (arr("scale_main", np.float64),
+                                                               arr("scale_text", np.float64),
+                                                               arr("scale_vision", np.float64))
+        desc.act = _lib.QSpec(iv["act_bits"], iv["act_sym"])
+        desc.weight = _lib.QSpec(iv["weight_bits"], iv["weight_sym"])
+        desc.aux_bits_floor = iv["aux_bits_floor"]
+        desc.use_cws, desc.use_mac = iv["use_cws"], iv["use_mac"]
+        desc.r_cws, desc.r_mac = iv["r_cws"], iv["r_mac"]
+        for name in _CODE_SETS:
+            setattr(desc, "q_" + name, arr("q_" + name, np.int8))
+            setattr(desc, "s_" + name, arr("s_" + name, np.float64))
         handle = C.c_void_p()
         _lib.check(lib.splitq_layer_create(C.byref(desc), int(dev.index or 0), C.byref(handle)))
         self.handle = handle
         self.device = dev
-        self.d_in, self.d_out = int(p.dim), d_out
+        self.d_in, self.d_out = iv["d_in"], iv["d_out"]
         self._ws = {}
         self._finalizer = weakref.finalize(self, lib.splitq_layer_destroy, handle)
 

@@ -177,8 +177,28 @@ def gen_mocd():
     save("mocd.npz", **out)
 
 
+def gen_layer_dir():
+    """A calibrated-layer directory written by the reference's save_layer
+    (layer.py:284-322; manifest.json + SPQT dumps, tensor.py:118-135), plus an
+    SPQT matrix and batch dump, and the layer's forward on its batch."""
+    import shutil
+    from modquant.tensor import save_tensor
+    d = os.path.join(HERE, "layer_dir")
+    shutil.rmtree(d, ignore_errors=True)
+    batch = generate(SynthConfig(tokens_text=24, tokens_vision=16, dim=48, vision_outlier_channels=(1, 7),
+                                 text_outlier_channels=(5, 30), seed=3))
+    w = generate_weight(48, 40, seed=10_003)
+    part = mocd.build_partition(batch, mocd.MocdConfig(ratio_vision=2 / 48, ratio_text=2 / 48))
+    layer = L.build_layer(w, batch, part, QuantSpec(4, False, Granularity.PER_TOKEN),
+                          QuantSpec(4, True, Granularity.PER_CHANNEL), use_cws=True, use_mac=True)
+    L.save_layer(layer, d)
+    save_tensor(os.path.join(d, "batch.spqt"), batch)
+    save_tensor(os.path.join(d, "matrix.spqt"), w[:5, :7])
+    np.save(os.path.join(d, "y_ref.npy"), L.forward(layer, batch))
+    print("wrote", d, sorted(os.listdir(d)))
+
+
 if __name__ == "__main__":
-    gen_quantizer()
-    gen_layers()
-    gen_config1()
-    gen_mocd()
+    which = sys.argv[1:] or ["quantizer", "layers", "config1", "mocd", "layer_dir"]
+    for name in which:
+        globals()["gen_" + name]()
