@@ -38,7 +38,8 @@
 
 namespace splitq {
 
-constexpr int KW_THREADS = 128;  // 4 row warps per CTA
+constexpr int KW_THREADS = 128;       // warp-per-row CTAs: 4 row warps
+constexpr int KW_THREADS_SYNC = 512;  // ... with a barrier per row round: 16 row warps
 
 #ifdef KW_TRACE  // phase clocks of CTA 0's first row (tools/k1_trace.py)
 #define KW_STAMP(i) \
@@ -488,8 +489,9 @@ struct KwZ {
 // chunks strided over all WPR x 32 threads; warp reductions are completed
 // across the group through SMEM (kw_gmin), the per-row parameters are
 // computed redundantly by every warp (deterministic) and stored by warp 0.
-template <typename T, bool SMF, int WPR>
-__global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(const K1Params p, int d_in) {
+template <typename T, bool SMF, int WPR, bool SYNC = false>
+__global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : KW_THREADS)
+    k1w_kernel(const K1Params p, int d_in) {
   static_assert(!(SMF && WPR > 1), "SMEM MAC fractions are per-warp rows");
   extern __shared__ __align__(16) uint8_t kw_smem[];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5, nwc = blockDim.x >> 5;
@@ -506,13 +508,23 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(co
   // pass A; the later passes read them there
   uint4* xs = reinterpret_cast<uint4*>(red + KW_RED_SITES * WPR * 8 + 2);
   float4* ds = reinterpret_cast<float4*>(xs + nchunks);
-  const int gw = WPR > 1 ? (int)blockIdx.x : (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  [[maybe_unused]] const int gw = WPR > 1 ? (int)blockIdx.x : (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nw = WPR > 1 ? (int)gridDim.x : (int)((gridDim.x * blockDim.x) >> 5);
   const bool cen = p.act.centered != 0, cena = p.aux.centered != 0;
   // dependents (the decode GEMVs) may launch now and prefetch their weights
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  for (int row = gw; row < p.T; row += nw) {
+  // rows: warp w of the grid takes rows w, w + #warps, ... (row groups: CTA b
+  // takes rows b, b + #CTAs, ...). The body is a do-while(0): `continue`
+  // ends the row. SYNC: a barrier per row round keeps the CTA's 16 warps in
+  // the same code region, so they share instruction-cache lines (the
+  // kernel is i-cache bound: `no_instruction` is its top stall). Measured
+  // at d_in = 3584: 0.695 -> 0.61 ms; at 18944 rows vary more and the
+  // barrier costs more than it saves (3.31 -> 4.6 ms), so it is not used.
+  const int rstep = WPR > 1 ? (int)gridDim.x : nw;
+  for (int rb = WPR > 1 ? (int)blockIdx.x : (int)(blockIdx.x * nwc); rb < p.T; rb += rstep) {
+    const int row = WPR > 1 ? rb : rb + wl;
     if constexpr (WPR > 1) __syncthreads();  // the previous row's SMEM reads are done
+    if (row < p.T) do {
     KW_STAMP(0)
     const T* xrow = reinterpret_cast<const T*>(p.x) + (int64_t)row * p.ldx;
     const uint4* xg = reinterpret_cast<const uint4*>(xrow);
@@ -945,6 +957,8 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : KW_THREADS) k1w_kernel(co
     }
     __syncwarp();
     KW_STAMP(15)
+    } while (0);
+    if constexpr (WPR == 1 && SYNC) __syncthreads();
   }
 }
 

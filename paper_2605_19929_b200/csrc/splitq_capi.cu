@@ -819,18 +819,18 @@ int launch_k1_dt(const K1Params& k, int d_in, cudaStream_t s) {
 // fp32 fast path with certified exact fp64 fallback (k1w.cuh).
 unsigned long long* k1w_trace_last = nullptr;
 
-template <typename T, bool SMF, int WPR>
+template <typename T, bool SMF, int WPR, bool SYNC = false>
 int launch_k1w_t(const K1Params& k, int d_in, int device, cudaStream_t stream) {
-  const int threads = WPR > 1 ? WPR * 32 : KW_THREADS;
+  const int threads = WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : KW_THREADS;
   const size_t smem = k1w_smem(d_in, threads / 32, SMF, WPR);
   static int attr_dev[64] = {0};
   if (device >= 0 && device < 64 && !attr_dev[device]) {
-    CUDA_TRY(cudaFuncSetAttribute(k1w_kernel<T, SMF, WPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_TRY(cudaFuncSetAttribute(k1w_kernel<T, SMF, WPR, SYNC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   200 * 1024));
     attr_dev[device] = 1;
   }
   int per_sm = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1w_kernel<T, SMF, WPR>, threads, smem));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1w_kernel<T, SMF, WPR, SYNC>, threads, smem));
   if (per_sm < 1) return SPLITQ_ERR_UNSUPPORTED;
   int64_t grid;
   if (WPR > 1) {  // one row per CTA
@@ -846,9 +846,9 @@ int launch_k1w_t(const K1Params& k, int d_in, int device, cudaStream_t stream) {
   K1Params kt = k;
   kt.trace = kw_trace_buf;
   k1w_trace_last = kw_trace_buf;
-  k1w_kernel<T, SMF, WPR><<<(unsigned)grid, threads, smem, stream>>>(kt, d_in);
+  k1w_kernel<T, SMF, WPR, SYNC><<<(unsigned)grid, threads, smem, stream>>>(kt, d_in);
 #else
-  k1w_kernel<T, SMF, WPR><<<(unsigned)grid, threads, smem, stream>>>(k, d_in);
+  k1w_kernel<T, SMF, WPR, SYNC><<<(unsigned)grid, threads, smem, stream>>>(k, d_in);
 #endif
   CUDA_TRY(cudaGetLastError());
   return SPLITQ_OK;
@@ -871,8 +871,12 @@ int launch_k1w(const K1Params& k, int d_in, int device, cudaStream_t stream) {
   if (grouped && !smf)
     return wpr_env >= 16 ? launch_k1w_t<T, false, 16>(k, d_in, device, stream)  // measured slower
                          : launch_k1w_t<T, false, 8>(k, d_in, device, stream);
-  return smf ? launch_k1w_t<T, true, 1>(k, d_in, device, stream)
-             : launch_k1w_t<T, false, 1>(k, d_in, device, stream);
+  if (smf) return launch_k1w_t<T, true, 1>(k, d_in, device, stream);
+  // row rounds with a CTA barrier (k1w.cuh): faster at d_in <= 8192
+  const char* senv = getenv("SPLITQ_K1_SYNC");
+  const bool sync = senv ? senv[0] == '1' : d_in <= 8192;
+  return sync ? launch_k1w_t<T, false, 1, true>(k, d_in, device, stream)
+              : launch_k1w_t<T, false, 1>(k, d_in, device, stream);
 }
 
 bool k1v3_eligible(const K1Params& k, int d_in) {

@@ -119,11 +119,14 @@ SHAPES = {
 }
 
 
-@pytest.fixture(params=["1", "8", "16"], ids=["warp_rows", "cta8_rows", "cta16_rows"], autouse=True)
+@pytest.fixture(params=[("1", "0"), ("1", "1"), ("8", "0"), ("16", "0")],
+                ids=["warp_rows", "warp_rows_sync", "cta8_rows", "cta16_rows"], autouse=True)
 def k1_row_group(request, monkeypatch):
-    """Every case runs with one warp per row (prefill) and with 8-warp row
-    groups (decode-sized calls); the library reads SPLITQ_K1_WPR per call."""
-    monkeypatch.setenv("SPLITQ_K1_WPR", request.param)
+    """Every case runs with one warp per row (prefill; with and without the
+    per-round CTA barrier) and with 8- / 16-warp row groups (decode-sized
+    calls); the library reads SPLITQ_K1_WPR / SPLITQ_K1_SYNC per call."""
+    monkeypatch.setenv("SPLITQ_K1_WPR", request.param[0])
+    monkeypatch.setenv("SPLITQ_K1_SYNC", request.param[1])
 
 
 @pytest.mark.parametrize("dt", DTS, ids=["f16", "bf16"])

@@ -1,0 +1,5 @@
+set -x
+mkdir -p gpurun_out
+timeout 300 python -m pytest tests/test_gpu_k1w.py tests/test_gpu_forward.py -x -q > gpurun_out/pytest_k1q.log 2>&1; rc=$?; echo rc=$rc
+[ $rc -eq 0 ] || exit 1
+timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --schedule serial > gpurun_out/bench_k1q.log 2>&1; echo rc=$?
