@@ -310,27 +310,238 @@ struct PairwiseStream {
   }
 };
 
-constexpr int TS_THREADS = 128;
+constexpr int TS_THREADS = 256;
 constexpr int TS_KMAX = 8;
+
+// One leaf of numpy's pairwise sum (<= 128 terms): 8 accumulators over the
+// body, combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the remainder
+// added in order (PairwiseStream::push without the tree above the leaf).
+struct LeafAcc {
+  double r[8];
+  double res;
+  int m, i;
+  __device__ void init(int len) {
+    m = len;
+    i = 0;
+    res = 0.0;
+  }
+  __device__ void push(double v) {
+    if (m < 8) {
+      res += v;
+    } else {
+      const int body = m - m % 8;
+      if (i < 8) r[i] = v;
+      else if (i < body) r[i & 7] += v;
+      else {
+        if (i == body) res = PairwiseStream::combine8(r);
+        res += v;
+      }
+      if (i == m - 1 && body == m) res = PairwiseStream::combine8(r);
+    }
+    ++i;
+  }
+};
+
+// Parallel exact pairwise sums of member sequences in token order.
+//
+// The reference sums cluster members (and the final squared deviations) with
+// numpy's pairwise algorithm over the members in token order. Its tree
+// depends only on the member count m: leaves of <= 128 consecutive members
+// (>= 64 once m > 128), combined by a fixed recursion. Here, per pass:
+//   (1) every thread counts the members of each cluster in its contiguous
+//       token segment; a per-cluster scan over the segments gives each
+//       segment's first member index;
+//   (2) one lane per cluster enumerates the cluster's leaves (PairwiseStream
+//       descent) into SMEM;
+//   (3) all threads compute leaf sums: a thread takes a contiguous run of
+//       leaves, locates the first member's token through the segment bases
+//       and scans forward, pushing members into the leaf accumulator;
+//   (4) one lane per cluster folds the leaf sums in order through the same
+//       PairwiseStream combine (finish_leaf) -- bit-identical to the serial
+//       stream, at ~n / 256 token steps per thread instead of n.
+struct TsShared {
+  int* seg;          // [TS_THREADS][TS_KMAX] member counts -> exclusive bases
+  int* lstart;       // [lcap] leaf first-member index
+  int* llen;         // [lcap]
+  double* lsum;      // [lcap]
+  int lofs[TS_KMAX + 1];  // first leaf slot per cluster
+  int lused[TS_KMAX];     // leaves per cluster
+  int lcum[TS_KMAX + 1];  // prefix of lused (the concatenated leaf list)
+  int nj[TS_KMAX];
+  double tot[TS_KMAX];
+};
+
+// Member test and value of token i for pass `mode`:
+//   0: cluster j members (asg[v] == j), value v / nc
+//   1: every token, value (v / nc - cen[asg[v]])^2           (final variance)
+//   2: every token, value v / nc                             (np.var: sum)
+//   3: every token, value (v / nc - cen[0])^2                (np.var: deviations)
+template <int MODE>
+__device__ __forceinline__ bool ts_member(int v, const int8_t* asg, int j) {
+  return MODE != 0 || asg[v] == j;
+}
+template <int MODE>
+__device__ __forceinline__ double ts_value(int v, double nc, const int8_t* asg, const double* cen) {
+  const double x = (double)v / nc;
+  if (MODE == 0 || MODE == 2) return x;
+  const double d = x - (MODE == 1 ? cen[asg[v]] : cen[0]);
+  return d * d;
+}
+
+// Runs the four steps for clusters 0..nk-1 (MODE 0) or for the single
+// all-token sequence (MODE 1-3, nk = 1); results in sh.tot[j] and sh.nj[j].
+template <int MODE>
+__device__ void ts_pairwise_pass(const uint16_t* col, int n, int nk, double nc, const int8_t* asg,
+                                 const double* cen, TsShared& sh) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int S = (n + TS_THREADS - 1) / TS_THREADS;
+  const int t0 = min(n, tid * S), t1 = min(n, t0 + S);
+  // (1) per-segment member counts
+  int cnt[TS_KMAX];
+#pragma unroll
+  for (int j = 0; j < TS_KMAX; ++j) cnt[j] = 0;
+  if (MODE == 0) {
+    for (int i = t0; i < t1; ++i) {
+      const int a = asg[col[i]];
+#pragma unroll
+      for (int j = 0; j < TS_KMAX; ++j) cnt[j] += a == j;
+    }
+  } else {
+    cnt[0] = t1 - t0;
+  }
+#pragma unroll
+  for (int j = 0; j < TS_KMAX; ++j) sh.seg[tid * TS_KMAX + j] = cnt[j];
+  __syncthreads();
+  if (warp < nk) {  // warp j: exclusive scan of cluster j's counts over the segments
+    const int j = warp;
+    constexpr int PER = TS_THREADS / 32;
+    int v[PER], run = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) v[q] = sh.seg[(lane * PER + q) * TS_KMAX + j], run += v[q];
+    int inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    int base = inc - run;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) sh.seg[(lane * PER + q) * TS_KMAX + j] = base, base += v[q];
+    if (lane == 31) sh.nj[j] = inc;
+  }
+  __syncthreads();
+  if (tid == 0) {  // leaf slots per cluster (a split leaf holds >= 64 members)
+    int o = 0;
+    for (int j = 0; j < nk; ++j) sh.lofs[j] = o, o += sh.nj[j] / 64 + 1;
+    sh.lofs[nk] = o;
+  }
+  __syncthreads();
+  // (2) leaf lists
+  if (warp < nk && lane == 0) {
+    const int j = warp, m = sh.nj[j];
+    int o = sh.lofs[j], st = 0;
+    if (m > 0) {
+      PairwiseStream ps;
+      ps.init(m);
+      while (!ps.done) {
+        sh.lstart[o] = st;
+        sh.llen[o] = ps.leaf_len;
+        st += ps.leaf_len;
+        ++o;
+        ps.finish_leaf(0.0);
+      }
+    }
+    sh.lused[j] = o - sh.lofs[j];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int c = 0;
+    for (int j = 0; j < nk; ++j) sh.lcum[j] = c, c += sh.lused[j];
+    sh.lcum[nk] = c;
+  }
+  __syncthreads();
+  // (3) leaf sums: thread tid takes leaves [L tid / T, L (tid + 1) / T) of the
+  // concatenated per-cluster lists
+  const int L = sh.lcum[nk];
+  const int a0 = (int)((int64_t)L * tid / TS_THREADS), a1 = (int)((int64_t)L * (tid + 1) / TS_THREADS);
+  int cur_j = -1, tok = 0, seen = 0;  // scan state: next token to read, members of cur_j before it
+  for (int a = a0; a < a1; ++a) {
+    int j = 0;
+    while (j + 1 < nk && sh.lcum[j + 1] <= a) ++j;
+    const int slot = sh.lofs[j] + (a - sh.lcum[j]);
+    const int ls = sh.lstart[slot], len = sh.llen[slot];
+    if (j != cur_j || seen != ls) {  // locate member ls of cluster j
+      int lo = 0, hi = TS_THREADS - 1;  // last segment whose base <= ls
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sh.seg[mid * TS_KMAX + j] <= ls) lo = mid;
+        else hi = mid - 1;
+      }
+      tok = min(n, lo * S);
+      seen = sh.seg[lo * TS_KMAX + j];
+      while (seen < ls) {
+        if (ts_member<MODE>(col[tok], asg, j)) ++seen;
+        ++tok;
+      }
+      cur_j = j;
+    }
+    LeafAcc acc;
+    acc.init(len);
+    int got = 0;
+    while (got < len) {
+      const int v = col[tok++];
+      if (ts_member<MODE>(v, asg, j)) {
+        acc.push(ts_value<MODE>(v, nc, asg, cen));
+        ++got;
+      }
+    }
+    seen += len;
+    sh.lsum[slot] = acc.res;
+  }
+  __syncthreads();
+  // (4) fold the leaf sums in order (PairwiseStream's combine)
+  if (warp < nk && lane == 0) {
+    const int j = warp, m = sh.nj[j];
+    double total = 0.0;
+    if (m > 0) {
+      PairwiseStream ps;
+      ps.init(m);
+      for (int q = 0; q < sh.lused[j]; ++q) ps.finish_leaf(sh.lsum[sh.lofs[j] + q]);
+      total = ps.total;
+    }
+    sh.tot[j] = total;
+  }
+  __syncthreads();
+}
 
 // One CTA per candidate channel c (c0 + blockIdx.x). counts_t: [n_cand x ld] uint16.
 __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
     const uint16_t* counts_t, int64_t ld, int n_cand, int n_text, int k_req, int max_iter, int c0,
     int c1, double* scores) {
   extern __shared__ __align__(16) uint8_t ts_smem[];
-  int* hist = reinterpret_cast<int*>(ts_smem);             // [n_cand + 1] -> cumulative
-  int8_t* asg = reinterpret_cast<int8_t*>(hist + n_cand + 1);  // [n_cand + 1] level -> cluster
+  const int lcap = n_text / 64 + TS_KMAX + 1;
+  double* lsum = reinterpret_cast<double*>(ts_smem);                       // [lcap]
+  int* hist = reinterpret_cast<int*>(lsum + lcap);                         // [n_cand + 1] -> cumulative
+  int* seg = hist + (n_cand + 1);                                          // [TS_THREADS x TS_KMAX]
+  int* lstart = seg + TS_THREADS * TS_KMAX;                                // [lcap]
+  int* llen = lstart + lcap;                                               // [lcap]
+  int8_t* asg = reinterpret_cast<int8_t*>(llen + lcap);                    // [n_cand + 1] level -> cluster
+  __shared__ TsShared sh;
   __shared__ double centers[TS_KMAX], new_centers[TS_KMAX];
-  __shared__ int n_j[TS_KMAX];
   __shared__ int distinct, changed;
-  __shared__ double result;
   const int c = c0 + blockIdx.x;
   if (c >= c1) return;
   const uint16_t* col = counts_t + (int64_t)c * ld;
   const int tid = threadIdx.x;
   const double nc = (double)n_cand;
+  if (tid == 0) {
+    sh.seg = seg;
+    sh.lstart = lstart;
+    sh.llen = llen;
+    sh.lsum = lsum;
+  }
 
-  for (int v = tid; v <= n_cand; v += TS_THREADS) hist[v] = 0;
+  for (int v = tid; v <= n_cand; v += TS_THREADS) hist[v] = 0, asg[v] = 0;
   if (tid == 0) distinct = 0;
   __syncthreads();
   for (int i = tid; i < n_text; i += TS_THREADS) atomicAdd(&hist[col[i]], 1);
@@ -352,18 +563,11 @@ __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
 
   if (k <= 1) {
     // np.var(values): mean = sum / n, then mean((v - mean)^2) (pairwise sums)
-    if (tid == 0) {
-      PairwiseStream ps;
-      ps.init(n);
-      for (int i = 0; i < n; ++i) ps.push((double)col[i] / nc);
-      const double mean = ps.total / (double)n;
-      ps.init(n);
-      for (int i = 0; i < n; ++i) {
-        const double d = (double)col[i] / nc - mean;
-        ps.push(d * d);
-      }
-      scores[c] = ps.total / (double)n;
-    }
+    ts_pairwise_pass<2>(col, n, 1, nc, asg, centers, sh);
+    if (tid == 0) centers[0] = sh.tot[0] / (double)n;
+    __syncthreads();
+    ts_pairwise_pass<3>(col, n, 1, nc, asg, centers, sh);
+    if (tid == 0) scores[c] = sh.tot[0] / (double)n;
     return;
   }
 
@@ -414,44 +618,19 @@ __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
   assign_levels(centers, false);
   __syncthreads();
   for (int it = 0; it < max_iter; ++it) {
-    if (tid < k) n_j[tid] = 0;
     if (tid == 0) changed = 0;
-    __syncthreads();
-    for (int v = tid; v <= n_cand; v += TS_THREADS) {
-      const int h = hist[v] - (v ? hist[v - 1] : 0);
-      if (h) atomicAdd(&n_j[asg[v]], h);
-    }
-    __syncthreads();
-    if (tid < k) {  // members.mean() in token order (numpy pairwise)
-      double cj = centers[tid];
-      if (n_j[tid] > 0) {
-        PairwiseStream ps;
-        ps.init(n_j[tid]);
-        for (int i = 0; i < n; ++i) {
-          const int v = col[i];
-          if (asg[v] == tid) ps.push((double)v / nc);
-        }
-        cj = ps.total / (double)n_j[tid];
-      }
-      new_centers[tid] = cj;
-    }
+    // members.mean() per cluster in token order (numpy pairwise), in parallel
+    ts_pairwise_pass<0>(col, n, k, nc, asg, centers, sh);
+    if (tid < k) new_centers[tid] = sh.nj[tid] > 0 ? sh.tot[tid] / (double)sh.nj[tid] : centers[tid];
     __syncthreads();
     assign_levels(new_centers, true);
     if (tid < k) centers[tid] = new_centers[tid];
     __syncthreads();
     if (!changed) break;
   }
-  if (tid == 0) {  // mean((values - centers[assign])^2)
-    PairwiseStream ps;
-    ps.init(n);
-    for (int i = 0; i < n; ++i) {
-      const int v = col[i];
-      const double d = (double)v / nc - centers[asg[v]];
-      ps.push(d * d);
-    }
-    result = ps.total / (double)n;
-    scores[c] = result;
-  }
+  // mean((values - centers[assign])^2)
+  ts_pairwise_pass<1>(col, n, 1, nc, asg, centers, sh);
+  if (tid == 0) scores[c] = sh.tot[0] / (double)n;
 }
 
 // ---------------------------------------------------------------- top-k
@@ -580,7 +759,8 @@ int splitq_mocd_text_score(const uint16_t* counts_t, int64_t ld, int64_t n_cand,
   if (k > n_text) return mfail(SPLITQ_ERR_INVALID, "cluster count exceeds number of text tokens");
   if (k > TS_KMAX) return mfail(SPLITQ_ERR_UNSUPPORTED, "at most 8 clusters on the GPU path");
   if (c1 <= c0) return SPLITQ_OK;
-  const size_t smem = (size_t)(n_cand + 1) * 4 + (size_t)(n_cand + 1);
+  const int64_t lcap = n_text / 64 + TS_KMAX + 1;
+  const size_t smem = (size_t)lcap * 16 + (size_t)(n_cand + 1) * 5 + (size_t)TS_THREADS * TS_KMAX * 4 + 16;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(mocd_text_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -45,7 +45,10 @@ def test_golden_mocd_cases():
 @pytest.mark.parametrize("seed,n_text,n_vis,dim,k,dtype", [
     (0, 300, 100, 96, 3, np.float32), (1, 1000, 200, 257, 3, np.float16),
     (2, 129, 40, 64, 2, np.float64), (3, 700, 100, 130, 4, np.float32),
-    (4, 64, 64, 40, 1, np.float32), (5, 2000, 500, 512, 3, np.float16)])
+    (4, 64, 64, 40, 1, np.float32), (5, 2000, 500, 512, 3, np.float16),
+    # long member sequences: many pairwise leaves per cluster (parallel exact sums)
+    (6, 30000, 1000, 24, 3, np.float16), (7, 20000, 100, 16, 1, np.float32),
+    (9, 25000, 500, 20, 8, np.float32)])
 def test_random_batches_bit_exact(seed, n_text, n_vis, dim, k, dtype):
     pkg, mg = _pkg()
     rng = np.random.default_rng(seed)
