@@ -10,7 +10,8 @@
 //               numpy 'linear' quantile init, per-level nearest-centre
 //               assignment (ties to the lower index), centre means and the final
 //               variance as numpy pairwise sums over the members in token order
-//               (streamed, PairwiseStream below), so scores are bit-identical
+//               (one subtree of the pairwise tree per thread, ts_pairwise_pass
+//               below), so scores are bit-identical
 //   topk        select_topk (mocd.py:80-89): k largest, ties to the lower index
 // Multi-GPU (mocd_gpu.py): absmax is MAX-all-reduced, the integer rank counts
 // are all-gathered in token order and channels are sharded for text_score.
@@ -236,142 +237,48 @@ __global__ void transpose_u16_kernel(const uint16_t* in, int64_t rows, int64_t c
 }
 
 // ---------------------------------------------------------------- exact k-means
-// numpy float64 pairwise summation of a stream of known length (see
-// oracle/mocd_oracle.py PairwiseStream for the reference-checked model).
-struct PairwiseStream {
-  int len_[24], n2_[24], phase_[24];
-  double left_[24];
-  int depth;
-  int leaf_len, leaf_i;
-  double r[8];
-  double res;
-  double total;
-  bool done;
+// numpy float64 pairwise summation (oracle/mocd_oracle.py pairwise_sum /
+// PairwiseStream are the reference-checked models).
+// numpy's 8-accumulator combine of a pairwise-sum leaf
+__device__ __forceinline__ double ts_combine8(const double* r) {
+  return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+}
 
-  __device__ void init(int n) {
-    depth = 0;
-    done = false;
-    total = 0.0;
-    if (n == 0) {
-      done = true;
-      return;
-    }
-    descend(n);
-  }
-  __device__ void descend(int m) {
-    while (m > 128) {
-      int n2 = m / 2;
-      n2 -= n2 % 8;
-      len_[depth] = m;
-      n2_[depth] = n2;
-      phase_[depth] = 0;
-      left_[depth] = 0.0;
-      ++depth;
-      m = n2;
-    }
-    leaf_len = m;
-    leaf_i = 0;
-    res = 0.0;
-  }
-  __device__ static double combine8(const double* r) {
-    return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-  }
-  __device__ void push(double v) {
-    const int m = leaf_len, i = leaf_i;
-    if (m < 8) {
-      res += v;
-    } else {
-      const int body = m - m % 8;
-      if (i < 8) r[i] = v;
-      else if (i < body) r[i & 7] += v;
-      else {
-        if (i == body) res = combine8(r);
-        res += v;
-      }
-      if (i == m - 1 && body == m) res = combine8(r);
-    }
-    leaf_i = i + 1;
-    if (leaf_i == m) finish_leaf(res);
-  }
-  __device__ void finish_leaf(double s) {
-    while (depth > 0) {
-      const int f = depth - 1;
-      if (phase_[f] == 0) {
-        phase_[f] = 1;
-        left_[f] = s;
-        descend(len_[f] - n2_[f]);
-        return;
-      }
-      s = left_[f] + s;
-      --depth;
-    }
-    total = s;
-    done = true;
-  }
-};
-
-constexpr int TS_THREADS = 256;
+constexpr int TS_THREADS = 512;
 constexpr int TS_KMAX = 8;
-
-// One leaf of numpy's pairwise sum (<= 128 terms): 8 accumulators over the
-// body, combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the remainder
-// added in order (PairwiseStream::push without the tree above the leaf).
-struct LeafAcc {
-  double r[8];
-  double res;
-  int m, i;
-  __device__ void init(int len) {
-    m = len;
-    i = 0;
-    res = 0.0;
-  }
-  __device__ void push(double v) {
-    if (m < 8) {
-      res += v;
-    } else {
-      const int body = m - m % 8;
-      if (i < 8) r[i] = v;
-      else if (i < body) r[i & 7] += v;
-      else {
-        if (i == body) res = PairwiseStream::combine8(r);
-        res += v;
-      }
-      if (i == m - 1 && body == m) res = PairwiseStream::combine8(r);
-    }
-    ++i;
-  }
-};
 
 // Parallel exact pairwise sums of member sequences in token order.
 //
 // The reference sums cluster members (and the final squared deviations) with
 // numpy's pairwise algorithm over the members in token order. Its tree
-// depends only on the member count m: leaves of <= 128 consecutive members
-// (>= 64 once m > 128), combined by a fixed recursion. Here, per pass:
-//   (1) every thread counts the members of each cluster in its contiguous
-//       token segment; a per-cluster scan over the segments gives each
-//       segment's first member index;
-//   (2) one lane per cluster enumerates the cluster's leaves (PairwiseStream
-//       descent) into SMEM;
-//   (3) all threads compute leaf sums: a thread takes a contiguous run of
-//       leaves, locates the first member's token through the segment bases
-//       and scans forward, pushing members into the leaf accumulator;
-//   (4) one lane per cluster folds the leaf sums in order through the same
-//       PairwiseStream combine (finish_leaf) -- bit-identical to the serial
-//       stream, at ~n / 256 token steps per thread instead of n.
+// depends only on the member count m: a node of more than 128 terms splits
+// into n2 = (m/2) & ~7 and m - n2; a node of at most 128 is a leaf (8
+// accumulators, then the remainder). With T = 2^D threads, thread t takes the
+// subtree reached from the root by the D bits of t (or nothing, when a leaf
+// is reached early and t's remaining bits are not zero), sums it sequentially
+// with the same recursion (ts_subtree), and the D top levels are folded
+// in SMEM level by level, left + right -- bit-identical to the serial sum.
+// A pass first counts each cluster's members in every thread's contiguous
+// token segment; the scanned counts locate a subtree's first member.
+#ifdef TS_TRACE  // cycles per pass step, printed by channel 0 (debug builds)
+__device__ unsigned long long ts_trace[8];
+#define TS_T0() long long _t = clock64();
+#define TS_T(i) if (threadIdx.x == 0 && blockIdx.x == 0) { long long _n = clock64(); ts_trace[i] += _n - _t; _t = _n; }
+#else
+#define TS_T0()
+#define TS_T(i)
+#endif
+constexpr int TS_DEPTH = 9;  // log2(TS_THREADS)
+static_assert((1 << TS_DEPTH) == TS_THREADS, "one subtree per thread");
+
 struct TsShared {
   int* seg;          // [TS_THREADS][TS_KMAX] member counts -> exclusive bases
-  int* lstart;       // [lcap] leaf first-member index
-  int* llen;         // [lcap]
-  double* lsum;      // [lcap]
-  int lofs[TS_KMAX + 1];  // first leaf slot per cluster
-  int lused[TS_KMAX];     // leaves per cluster
-  int lcum[TS_KMAX + 1];  // prefix of lused (the concatenated leaf list)
+  double* val;       // [TS_THREADS] subtree sums
   int nj[TS_KMAX];
   double tot[TS_KMAX];
 };
 
-// Member test and value of token i for pass `mode`:
+// Member test and value of token value v for pass `mode`:
 //   0: cluster j members (asg[v] == j), value v / nc
 //   1: every token, value (v / nc - cen[asg[v]])^2           (final variance)
 //   2: every token, value v / nc                             (np.var: sum)
@@ -385,133 +292,195 @@ __device__ __forceinline__ double ts_value(int v, double nc, const int8_t* asg, 
   const double x = (double)v / nc;
   if (MODE == 0 || MODE == 2) return x;
   const double d = x - (MODE == 1 ? cen[asg[v]] : cen[0]);
-  return d * d;
+  return __dmul_rn(d, d);  // numpy squares first, then sums: no FMA contraction
 }
 
-// Runs the four steps for clusters 0..nk-1 (MODE 0) or for the single
-// all-token sequence (MODE 1-3, nk = 1); results in sh.tot[j] and sh.nj[j].
+// Sequential token reader: 16-byte loads (8 tokens) when the row is aligned.
+struct TokReader {
+  const uint16_t* col;
+  int pos;
+  bool vec;
+  uint4 buf;
+  __device__ void start(const uint16_t* c, int p, bool v) {
+    col = c;
+    pos = p;
+    vec = v;
+    if (vec && (pos & 7)) buf = __ldg(reinterpret_cast<const uint4*>(col) + (pos >> 3));
+  }
+  __device__ __forceinline__ int next() {
+    if (!vec) return col[pos++];
+    if ((pos & 7) == 0) buf = __ldg(reinterpret_cast<const uint4*>(col) + (pos >> 3));
+    const int q = pos & 7;
+    const uint32_t w = q < 2 ? buf.x : q < 4 ? buf.y : q < 6 ? buf.z : buf.w;
+    ++pos;
+    return (int)((q & 1) ? (w >> 16) : (w & 0xFFFFu));
+  }
+};
+
+// Pairwise sum of the next m member values from the reader (numpy recursion).
+template <int MODE>
+__device__ double ts_subtree(TokReader& rd, int m, int j, double nc, const int8_t* asg, const double* cen) {
+  auto next = [&]() -> double {
+    int v = rd.next();
+    while (!ts_member<MODE>(v, asg, j)) v = rd.next();
+    return ts_value<MODE>(v, nc, asg, cen);
+  };
+  auto leaf = [&](int len) -> double {
+    double res = 0.0;
+    if (len < 8) {
+      for (int q = 0; q < len; ++q) res += next();
+      return res;
+    }
+    double r[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) r[u] = next();
+    const int body = len - len % 8;
+    for (int q = 8; q < body; q += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) r[u] += next();
+    }
+    res = ts_combine8(r);
+    for (int q = body; q < len; ++q) res += next();
+    return res;
+  };
+  if (m <= 128) return leaf(m);
+  // explicit recursion: pending right-subtree lengths and left sums
+  int len_[24], n2_[24], ph_[24];
+  double left_[24];
+  int d = 0, cur = m;
+  double s;
+  for (;;) {
+    while (cur > 128) {
+      int n2 = cur / 2;
+      n2 -= n2 % 8;
+      len_[d] = cur, n2_[d] = n2, ph_[d] = 0;
+      ++d;
+      cur = n2;
+    }
+    s = leaf(cur);
+    while (d > 0 && ph_[d - 1] == 1) {
+      --d;
+      s = left_[d] + s;
+    }
+    if (d == 0) return s;
+    ph_[d - 1] = 1;
+    left_[d - 1] = s;
+    cur = len_[d - 1] - n2_[d - 1];
+  }
+}
+
+// Exact pairwise sums for clusters 0..nk-1 (MODE 0) or the single all-token
+// sequence (MODE 1-3, nk = 1): results in sh.tot[j] and sh.nj[j].
 template <int MODE>
 __device__ void ts_pairwise_pass(const uint16_t* col, int n, int nk, double nc, const int8_t* asg,
-                                 const double* cen, TsShared& sh) {
+                                 const double* cen, TsShared& sh, bool vec) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int S = (n + TS_THREADS - 1) / TS_THREADS;
+  const int S = ((n + TS_THREADS - 1) / TS_THREADS + 7) & ~7;  // segments of whole 16-byte vectors
   const int t0 = min(n, tid * S), t1 = min(n, t0 + S);
-  // (1) per-segment member counts
-  int cnt[TS_KMAX];
-#pragma unroll
-  for (int j = 0; j < TS_KMAX; ++j) cnt[j] = 0;
+  TS_T0()
   if (MODE == 0) {
+    // per-segment member counts, scanned per cluster over the segments
+    int cnt[TS_KMAX];
+#pragma unroll
+    for (int j = 0; j < TS_KMAX; ++j) cnt[j] = 0;
+    TokReader rd;
+    rd.start(col, t0, vec);
     for (int i = t0; i < t1; ++i) {
-      const int a = asg[col[i]];
+      const int a = asg[rd.next()];
 #pragma unroll
       for (int j = 0; j < TS_KMAX; ++j) cnt[j] += a == j;
     }
-  } else {
-    cnt[0] = t1 - t0;
-  }
 #pragma unroll
-  for (int j = 0; j < TS_KMAX; ++j) sh.seg[tid * TS_KMAX + j] = cnt[j];
-  __syncthreads();
-  if (warp < nk) {  // warp j: exclusive scan of cluster j's counts over the segments
-    const int j = warp;
-    constexpr int PER = TS_THREADS / 32;
-    int v[PER], run = 0;
+    for (int j = 0; j < TS_KMAX; ++j) sh.seg[tid * TS_KMAX + j] = cnt[j];
+    __syncthreads();
+    if (warp < nk) {  // warp j: exclusive scan of cluster j's counts
+      const int j = warp;
+      constexpr int PER = TS_THREADS / 32;
+      int v[PER], run = 0;
 #pragma unroll
-    for (int q = 0; q < PER; ++q) v[q] = sh.seg[(lane * PER + q) * TS_KMAX + j], run += v[q];
-    int inc = run;
+      for (int q = 0; q < PER; ++q) v[q] = sh.seg[(lane * PER + q) * TS_KMAX + j], run += v[q];
+      int inc = run;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += y;
-    }
-    int base = inc - run;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      int base = inc - run;
 #pragma unroll
-    for (int q = 0; q < PER; ++q) sh.seg[(lane * PER + q) * TS_KMAX + j] = base, base += v[q];
-    if (lane == 31) sh.nj[j] = inc;
-  }
-  __syncthreads();
-  if (tid == 0) {  // leaf slots per cluster (a split leaf holds >= 64 members)
-    int o = 0;
-    for (int j = 0; j < nk; ++j) sh.lofs[j] = o, o += sh.nj[j] / 64 + 1;
-    sh.lofs[nk] = o;
-  }
-  __syncthreads();
-  // (2) leaf lists
-  if (warp < nk && lane == 0) {
-    const int j = warp, m = sh.nj[j];
-    int o = sh.lofs[j], st = 0;
-    if (m > 0) {
-      PairwiseStream ps;
-      ps.init(m);
-      while (!ps.done) {
-        sh.lstart[o] = st;
-        sh.llen[o] = ps.leaf_len;
-        st += ps.leaf_len;
-        ++o;
-        ps.finish_leaf(0.0);
-      }
+      for (int q = 0; q < PER; ++q) sh.seg[(lane * PER + q) * TS_KMAX + j] = base, base += v[q];
+      if (lane == 31) sh.nj[j] = inc;
     }
-    sh.lused[j] = o - sh.lofs[j];
+  } else if (tid == 0) {
+    sh.nj[0] = n;
   }
   __syncthreads();
-  if (tid == 0) {
-    int c = 0;
-    for (int j = 0; j < nk; ++j) sh.lcum[j] = c, c += sh.lused[j];
-    sh.lcum[nk] = c;
-  }
-  __syncthreads();
-  // (3) leaf sums: thread tid takes leaves [L tid / T, L (tid + 1) / T) of the
-  // concatenated per-cluster lists
-  const int L = sh.lcum[nk];
-  const int a0 = (int)((int64_t)L * tid / TS_THREADS), a1 = (int)((int64_t)L * (tid + 1) / TS_THREADS);
-  int cur_j = -1, tok = 0, seen = 0;  // scan state: next token to read, members of cur_j before it
-  for (int a = a0; a < a1; ++a) {
-    int j = 0;
-    while (j + 1 < nk && sh.lcum[j + 1] <= a) ++j;
-    const int slot = sh.lofs[j] + (a - sh.lcum[j]);
-    const int ls = sh.lstart[slot], len = sh.llen[slot];
-    if (j != cur_j || seen != ls) {  // locate member ls of cluster j
-      int lo = 0, hi = TS_THREADS - 1;  // last segment whose base <= ls
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (sh.seg[mid * TS_KMAX + j] <= ls) lo = mid;
-        else hi = mid - 1;
+  TS_T(0)
+  for (int j = 0; j < nk; ++j) {
+    const int m = sh.nj[j];
+    // this thread's subtree: the D bits of tid from the root
+    int st = 0, len = m;
+    bool own = m > 0;
+    for (int l = 0; l < TS_DEPTH && own; ++l) {
+      if (len <= 128) {  // a leaf above the thread level: its leftmost thread owns it
+        own = (tid & ((1 << (TS_DEPTH - l)) - 1)) == 0;
+        break;
       }
-      tok = min(n, lo * S);
-      seen = sh.seg[lo * TS_KMAX + j];
-      while (seen < ls) {
-        if (ts_member<MODE>(col[tok], asg, j)) ++seen;
-        ++tok;
+      int n2 = len / 2;
+      n2 -= n2 % 8;
+      if ((tid >> (TS_DEPTH - 1 - l)) & 1) st += n2, len -= n2;
+      else len = n2;
+    }
+    double v = 0.0;
+    if (own) {
+      // first member: token st (MODE != 0), else through the segment bases
+      int tok = st;
+      if (MODE == 0) {
+        int lo = 0, hi = TS_THREADS - 1;  // last segment whose base <= st
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (sh.seg[mid * TS_KMAX + j] <= st) lo = mid;
+          else hi = mid - 1;
+        }
+        int seen = sh.seg[lo * TS_KMAX + j];
+        TokReader rd;
+        rd.start(col, min(n, lo * S), vec);
+        while (seen < st)
+          if (ts_member<MODE>(rd.next(), asg, j)) ++seen;
+        tok = rd.pos;
       }
-      cur_j = j;
+      TokReader rd;
+      rd.start(col, tok, vec);
+      v = ts_subtree<MODE>(rd, len, j, nc, asg, cen);
     }
-    LeafAcc acc;
-    acc.init(len);
-    int got = 0;
-    while (got < len) {
-      const int v = col[tok++];
-      if (ts_member<MODE>(v, asg, j)) {
-        acc.push(ts_value<MODE>(v, nc, asg, cen));
-        ++got;
+    sh.val[tid] = v;
+    __syncthreads();
+    TS_T(1)
+    // fold the top D levels: node (l, p) = left slot p << (D - l) + right slot
+    for (int l = TS_DEPTH - 1; l >= 0; --l) {
+      if (tid < (1 << l)) {
+        int nl = m;  // node (l, tid) length: descend l levels
+        bool split = m > 0;
+        for (int q = 0; q < l && split; ++q) {
+          if (nl <= 128) {
+            split = false;
+            break;
+          }
+          int n2 = nl / 2;
+          n2 -= n2 % 8;
+          nl = ((tid >> (l - 1 - q)) & 1) ? nl - n2 : n2;
+        }
+        if (split && nl > 128)
+          sh.val[tid << (TS_DEPTH - l)] = sh.val[tid << (TS_DEPTH - l)] + sh.val[(2 * tid + 1) << (TS_DEPTH - l - 1)];
       }
+      __syncthreads();
     }
-    seen += len;
-    sh.lsum[slot] = acc.res;
+    if (tid == 0) sh.tot[j] = sh.val[0];
+    __syncthreads();
+    TS_T(2)
   }
-  __syncthreads();
-  // (4) fold the leaf sums in order (PairwiseStream's combine)
-  if (warp < nk && lane == 0) {
-    const int j = warp, m = sh.nj[j];
-    double total = 0.0;
-    if (m > 0) {
-      PairwiseStream ps;
-      ps.init(m);
-      for (int q = 0; q < sh.lused[j]; ++q) ps.finish_leaf(sh.lsum[sh.lofs[j] + q]);
-      total = ps.total;
-    }
-    sh.tot[j] = total;
-  }
-  __syncthreads();
+#ifdef TS_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == 0) ts_trace[4] += 1;
+#endif
 }
 
 // One CTA per candidate channel c (c0 + blockIdx.x). counts_t: [n_cand x ld] uint16.
@@ -519,26 +488,22 @@ __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
     const uint16_t* counts_t, int64_t ld, int n_cand, int n_text, int k_req, int max_iter, int c0,
     int c1, double* scores) {
   extern __shared__ __align__(16) uint8_t ts_smem[];
-  const int lcap = n_text / 64 + TS_KMAX + 1;
-  double* lsum = reinterpret_cast<double*>(ts_smem);                       // [lcap]
-  int* hist = reinterpret_cast<int*>(lsum + lcap);                         // [n_cand + 1] -> cumulative
+  double* val = reinterpret_cast<double*>(ts_smem);                        // [TS_THREADS]
+  int* hist = reinterpret_cast<int*>(val + TS_THREADS);                    // [n_cand + 1] -> cumulative
   int* seg = hist + (n_cand + 1);                                          // [TS_THREADS x TS_KMAX]
-  int* lstart = seg + TS_THREADS * TS_KMAX;                                // [lcap]
-  int* llen = lstart + lcap;                                               // [lcap]
-  int8_t* asg = reinterpret_cast<int8_t*>(llen + lcap);                    // [n_cand + 1] level -> cluster
+  int8_t* asg = reinterpret_cast<int8_t*>(seg + TS_THREADS * TS_KMAX);     // [n_cand + 1] level -> cluster
   __shared__ TsShared sh;
   __shared__ double centers[TS_KMAX], new_centers[TS_KMAX];
   __shared__ int distinct, changed;
   const int c = c0 + blockIdx.x;
   if (c >= c1) return;
   const uint16_t* col = counts_t + (int64_t)c * ld;
+  const bool vec = (reinterpret_cast<uintptr_t>(col) & 15) == 0;  // 16-byte token loads
   const int tid = threadIdx.x;
   const double nc = (double)n_cand;
   if (tid == 0) {
     sh.seg = seg;
-    sh.lstart = lstart;
-    sh.llen = llen;
-    sh.lsum = lsum;
+    sh.val = val;
   }
 
   for (int v = tid; v <= n_cand; v += TS_THREADS) hist[v] = 0, asg[v] = 0;
@@ -563,10 +528,10 @@ __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
 
   if (k <= 1) {
     // np.var(values): mean = sum / n, then mean((v - mean)^2) (pairwise sums)
-    ts_pairwise_pass<2>(col, n, 1, nc, asg, centers, sh);
+    ts_pairwise_pass<2>(col, n, 1, nc, asg, centers, sh, vec);
     if (tid == 0) centers[0] = sh.tot[0] / (double)n;
     __syncthreads();
-    ts_pairwise_pass<3>(col, n, 1, nc, asg, centers, sh);
+    ts_pairwise_pass<3>(col, n, 1, nc, asg, centers, sh, vec);
     if (tid == 0) scores[c] = sh.tot[0] / (double)n;
     return;
   }
@@ -620,17 +585,24 @@ __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
   for (int it = 0; it < max_iter; ++it) {
     if (tid == 0) changed = 0;
     // members.mean() per cluster in token order (numpy pairwise), in parallel
-    ts_pairwise_pass<0>(col, n, k, nc, asg, centers, sh);
+    ts_pairwise_pass<0>(col, n, k, nc, asg, centers, sh, vec);
     if (tid < k) new_centers[tid] = sh.nj[tid] > 0 ? sh.tot[tid] / (double)sh.nj[tid] : centers[tid];
     __syncthreads();
     assign_levels(new_centers, true);
     if (tid < k) centers[tid] = new_centers[tid];
     __syncthreads();
-    if (!changed) break;
+    const int ch = changed;
+    __syncthreads();  // every thread has read the flag before thread 0 resets it
+    if (!ch) break;
   }
   // mean((values - centers[assign])^2)
-  ts_pairwise_pass<1>(col, n, 1, nc, asg, centers, sh);
+  ts_pairwise_pass<1>(col, n, 1, nc, asg, centers, sh, vec);
   if (tid == 0) scores[c] = sh.tot[0] / (double)n;
+#ifdef TS_TRACE
+  if (tid == 0 && blockIdx.x == 0)
+    printf("TS_TRACE n=%d k=%d passes=%llu count+scan=%llu subtrees=%llu fold=%llu\n", n, k,
+           ts_trace[4], ts_trace[0], ts_trace[1], ts_trace[2]);
+#endif
 }
 
 // ---------------------------------------------------------------- top-k
@@ -759,8 +731,7 @@ int splitq_mocd_text_score(const uint16_t* counts_t, int64_t ld, int64_t n_cand,
   if (k > n_text) return mfail(SPLITQ_ERR_INVALID, "cluster count exceeds number of text tokens");
   if (k > TS_KMAX) return mfail(SPLITQ_ERR_UNSUPPORTED, "at most 8 clusters on the GPU path");
   if (c1 <= c0) return SPLITQ_OK;
-  const int64_t lcap = n_text / 64 + TS_KMAX + 1;
-  const size_t smem = (size_t)lcap * 16 + (size_t)(n_cand + 1) * 5 + (size_t)TS_THREADS * TS_KMAX * 4 + 16;
+  const size_t smem = (size_t)TS_THREADS * 8 + (size_t)(n_cand + 1) * 5 + (size_t)TS_THREADS * TS_KMAX * 4 + 16;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(mocd_text_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -98,7 +98,9 @@ class GpuStats:
         lib = _lib.load()
         n_text = counts.shape[0]
         c1 = n_cand if c1 is None else c1
-        counts_t = torch.empty((n_cand, max(n_text, 1)), dtype=torch.int16, device=counts.device)
+        # rows padded to 8 tokens: the kernel reads them as 16-byte vectors
+        counts_t = torch.empty((n_cand, max((n_text + 7) // 8 * 8, 8)), dtype=torch.int16,
+                               device=counts.device)
         _lib.check(lib.splitq_mocd_transpose_u16(counts.data_ptr(), n_text, n_cand,
                                                  counts_t.data_ptr(), counts_t.stride(0), _stream()))
         scores = torch.zeros(n_cand, dtype=torch.float64, device=counts.device)
