@@ -56,6 +56,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-tokens", type=int, default=512)
     ap.add_argument("--out-dtype", default="float16", choices=["float16", "bfloat16", "float32"])
+    ap.add_argument("--model", default="7b", choices=["7b", "3b"],
+                    help="projection shapes: Qwen2.5-VL-7B (config 3/4, the headline) or -3B (config 2)")
+    ap.add_argument("--vision-frac", type=float, default=None,
+                    help="vision share of the tokens (default 1280/8192 for 7B, 3072/4096 for 3B)")
     ap.add_argument("--schedule", default="branches", choices=["serial", "branches"],
                     help="serial: the seven projections one after another on one stream; branches: "
                          "the decoder block's independent projections (q||k||v, o, gate||up, down) on "
@@ -120,13 +124,19 @@ def measured_peaks():
 
 # ------------------------------------------------------------------ workload
 
-def build_workload(pkg, tokens, abits, wbits, seed=0):
-    """Layer inputs (one per distinct projection input) and the 7 layers."""
+def build_workload(pkg, tokens, abits, wbits, seed=0, model="7b", vision_frac=None):
+    """Layer inputs (one per distinct projection input) and the 7 layers.
+    Samples of SEQ tokens (or one sample of `tokens`), each with its vision
+    tokens as contiguous image spans: 1280 of 8192 (config 3) by default,
+    3072 of 4096 for the 3B shapes (config 2)."""
     rng = np.random.default_rng(seed)
-    shape = wl.QWEN_7B
+    shape = wl.QWEN_3B if model == "3b" else wl.QWEN_7B
+    if vision_frac is None:
+        vision_frac = 0.75 if model == "3b" else VISION_PER_SAMPLE / SEQ
     specs = wl.model_specs(shape, abits=abits, wbits=wbits)
-    n_samples = max(1, tokens // SEQ)
-    tags = np.concatenate([wl.tags_with_spans(rng, SEQ, VISION_PER_SAMPLE)
+    seq = min(SEQ, tokens)
+    n_samples = max(1, tokens // seq)
+    tags = np.concatenate([wl.tags_with_spans(rng, seq, int(round(vision_frac * seq)))
                            for _ in range(n_samples)])[:tokens]
     if tags.shape[0] < tokens:  # non-multiple of SEQ
         tags = np.concatenate([tags, wl.tags_with_spans(rng, tokens - tags.shape[0],
@@ -236,7 +246,8 @@ def run_ours(args):
     lib = _lib.load()
     tokens = args.tokens  # per rank (weak scaling: every rank runs one batch)
     global_tokens = tokens * world
-    tags_all, inputs, layers = build_workload(pkg, tokens, args.abits, args.wbits)
+    tags_all, inputs, layers = build_workload(pkg, tokens, args.abits, args.wbits, model=args.model,
+                                              vision_frac=args.vision_frac)
     tags_np = np.ascontiguousarray(tags_all)
     tags = torch.from_numpy(tags_np).to(dev)
     xs = {g: make_input_tensor(torch, dev, tokens, inputs[g], tags_np, 1000 + 17 * rank + i)
@@ -359,8 +370,10 @@ def run_ours(args):
         "data": "synthetic (seeded N(0,1) fp16 activations with x30-x100 outlier channels; "
                 "random-init weights and low-rank factors)",
         "config": {
-            "workload": "config3: Qwen2.5-VL-7B decoder projections q,k,v,o,gate,up,down; W4A4 "
-                        "(A asym per-token, W sym per-channel), CWS+MAC on, K_t=K_v=32",
+            "workload": (f"config3: Qwen2.5-VL-7B decoder projections q,k,v,o,gate,up,down; W{args.wbits}A{args.abits} "
+                         "(A asym per-token, W sym per-channel), CWS+MAC on, K_t=K_v=32" if args.model == "7b" else
+                         f"config2: Qwen2.5-VL-3B decoder projections q,k,v,o,gate,up,down; W{args.wbits}A{args.abits} "
+                         "(A asym per-token, W sym per-channel), CWS+MAC on, K = 1% of D_in"),
             "global_tokens": global_tokens, "tokens_per_gpu": tokens,
             "samples": SAMPLES, "seq_len": SEQ, "vision_tokens_per_sample": VISION_PER_SAMPLE,
             "parallelism": f"token-sharded replicas x{world}, one 8x8192-token batch per rank "
@@ -529,7 +542,8 @@ def run_reference(args):
 
     cores = os.cpu_count() or 1
     tokens_sample = args.cpu_sample_tokens
-    tags_all, inputs, layers = build_workload(pkg, max(args.tokens, SEQ), args.abits, args.wbits)
+    tags_all, inputs, layers = build_workload(pkg, max(args.tokens, SEQ), args.abits, args.wbits,
+                                              model=args.model, vision_frac=args.vision_frac)
     rng = np.random.default_rng(7)
     tags = tags_all[:tokens_sample]
     xs = {}
