@@ -489,7 +489,7 @@ struct KwZ {
 // chunks strided over all WPR x 32 threads; warp reductions are completed
 // across the group through SMEM (kw_gmin), the per-row parameters are
 // computed redundantly by every warp (deterministic) and stored by warp 0.
-template <typename T, bool SMF, int WPR, bool SYNC = false>
+template <typename T, bool SMF, int WPR, bool SYNC = false, bool G64 = false>
 __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : KW_THREADS)
     k1w_kernel(const K1Params p, int d_in) {
   static_assert(!(SMF && WPR > 1), "SMEM MAC fractions are per-warp rows");
@@ -801,6 +801,13 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
       allx = k[0] == 0;
     }
     KW_STAMP(7)
+#ifdef KW_DEBUG  // fallback counters in the status block (tools/k1_debug.py)
+    if (lane == 0) {
+      atomicAdd(p.err + 1, qn);
+      if (allx) atomicAdd(p.err + 2, 1);
+      if (!c.safe) atomicAdd(p.err + 5, 1);
+    }
+#endif
     const int qnE = allx ? 0 : qn;
     const int nfix = 8 * (allx ? nchunks : qn);
     __syncwarp();
@@ -868,8 +875,8 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
     int zpe = 0;
     float ratio = 1.f;
     int use_smf = 0;
+    double rSe = 1.0;
     if (lane == 0) {
-      double rSe;
       if (!kw_params(elo64, ehi64, p.aux, &Se, &zpe, &rSe) && w0) atomicOr(p.err, ERR_SCALE_ZERO);
       // f carries |err| <= vmax 2^-22 in units of S (+ 2^-16 when read back from
       // the 16-bit SMEM copy): times S / Se in units of e / Se
@@ -888,6 +895,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
     }
     ce = kw_shfl(ce, 0);
     Se = kw_shfl_d(Se, 0);
+    if constexpr (G64) rSe = kw_shfl_d(rSe, 0);
     zpe = __shfl_sync(0xffffffffu, zpe, 0);
     ratio = __shfl_sync(0xffffffffu, ratio, 0);
     use_smf = __shfl_sync(0xffffffffu, use_smf, 0);
@@ -896,8 +904,53 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
     // ------------------------------------------------ pass G: MAC residual codes
     int8_t* erow = p.a_mac + (int64_t)slot * p.ld_main;
     qn = qnE;  // the chunks flagged in pass E are exact-coded here as well
-    const bool allg = allx || !ce.safe;
-    if (!allg) {
+    // fp64 pass G: when S / S_e is large (8-bit aux codes: ~255) the fp32
+    // residual f = v - n carries too few bits for the MAC code (measured: 14 %
+    // of chunks flagged, queue overflow on nearly every 18944-wide row). The
+    // residual is then formed as the reference does -- e = fl64(z - fl64(m S))
+    // with the exact main code m already in the row -- and e / S_e taken as
+    // e * (1 / S_e) (<= 2 fp64 roundings from the reference's quotient): only
+    // fractions within 2^-30 of one half are flagged for the exact division.
+    // (a separate instantiation, chosen on the host for wide aux codes: its
+    // registers would cost the 4-bit configurations occupancy)
+    const bool g64 = G64 && !SMF && !allx && (!ce.safe || ratio > 64.f);
+    const bool allg = allx || (!ce.safe && !g64);
+    if (g64) {
+      for (int j0 = 0; j0 < nchunks; j0 += GT) {
+        const int j = j0 + gl;
+        bool flag = false;
+        if (j < nchunks) {
+          float x[8], d[8];
+          kwl(j, x, d);
+          const uint2 cm = *reinterpret_cast<const uint2*>(arow + 8 * j);  // exact main codes (pass E + fixups)
+          const uint32_t cw[2] = {cm.x, cm.y};
+          const double2* d64 = reinterpret_cast<const double2*>(p.d_main + 8 * j);
+          uint32_t by[2] = {0u, 0u};
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const double2 dd = __ldg(d64 + h);
+#pragma unroll
+            for (int u2 = 0; u2 < 2; ++u2) {
+              const int u = 2 * h + u2;
+              const uint32_t byte = (cw[u >> 2] >> (8 * (u & 3))) & 0xFFu;
+              const int m = cen ? (int)(int8_t)byte : (int)byte - zp;  // q - zp
+              const double z64 = __dmul_rn((double)x[u], u2 ? dd.y : dd.x);
+              const double e64 = __dsub_rn(z64, __dmul_rn((double)m, S));
+              const double t = __dmul_rn(e64, rSe);
+              const double a = fabs(t);
+              const double fr = a - floor(a);
+              flag |= !(fabs(fr - 0.5) > 9.313225746154785e-10);  // 2^-30 (also catches NaN)
+              double qa = floor(a + 0.5);
+              int qe = (int)(t < 0.0 ? -qa : qa) + zpe;
+              qe = min(max(qe, p.aux.qmin), p.aux.qmax);
+              by[u >> 2] |= ((uint32_t)(cena ? qe - zpe : qe) & 0xFFu) << (8 * (u & 3));
+            }
+          }
+          *reinterpret_cast<uint2*>(erow + 8 * j) = make_uint2(by[0], by[1]);
+        }
+        kw_enqueue(q, qn, flag, j);
+      }
+    } else if (!allg) {
       for (int j0 = 0; j0 < nchunks; j0 += GT) {
         const int j = j0 + gl;
         bool flag = false;
@@ -947,6 +1000,13 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
       allg2 = k[0] == 0;
     }
     KW_STAMP(14)
+#ifdef KW_DEBUG
+    if (lane == 0) {
+      atomicAdd(p.err + 3, qn);
+      if (allg2) atomicAdd(p.err + 2, 1 << 16);
+      if (!ce.safe) atomicAdd(p.err + 6, 1);
+    }
+#endif
     const int ngix = 8 * (allg2 ? nchunks : qn);
     __syncwarp();
     for (int i = allg2 ? gl : lane; i < ngix; i += allg2 ? GT : 32) {

@@ -819,18 +819,18 @@ int launch_k1_dt(const K1Params& k, int d_in, cudaStream_t s) {
 // fp32 fast path with certified exact fp64 fallback (k1w.cuh).
 unsigned long long* k1w_trace_last = nullptr;
 
-template <typename T, bool SMF, int WPR, bool SYNC = false>
+template <typename T, bool SMF, int WPR, bool SYNC = false, bool G64 = false>
 int launch_k1w_t(const K1Params& k, int d_in, int device, cudaStream_t stream) {
   const int threads = WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : KW_THREADS;
   const size_t smem = k1w_smem(d_in, threads / 32, SMF, WPR);
   static int attr_dev[64] = {0};
   if (device >= 0 && device < 64 && !attr_dev[device]) {
-    CUDA_TRY(cudaFuncSetAttribute(k1w_kernel<T, SMF, WPR, SYNC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_TRY(cudaFuncSetAttribute(k1w_kernel<T, SMF, WPR, SYNC, G64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   200 * 1024));
     attr_dev[device] = 1;
   }
   int per_sm = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1w_kernel<T, SMF, WPR, SYNC>, threads, smem));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1w_kernel<T, SMF, WPR, SYNC, G64>, threads, smem));
   if (per_sm < 1) return SPLITQ_ERR_UNSUPPORTED;
   int64_t grid;
   if (WPR > 1) {  // one row per CTA
@@ -846,16 +846,16 @@ int launch_k1w_t(const K1Params& k, int d_in, int device, cudaStream_t stream) {
   K1Params kt = k;
   kt.trace = kw_trace_buf;
   k1w_trace_last = kw_trace_buf;
-  k1w_kernel<T, SMF, WPR, SYNC><<<(unsigned)grid, threads, smem, stream>>>(kt, d_in);
+  k1w_kernel<T, SMF, WPR, SYNC, G64><<<(unsigned)grid, threads, smem, stream>>>(kt, d_in);
 #else
-  k1w_kernel<T, SMF, WPR, SYNC><<<(unsigned)grid, threads, smem, stream>>>(k, d_in);
+  k1w_kernel<T, SMF, WPR, SYNC, G64><<<(unsigned)grid, threads, smem, stream>>>(k, d_in);
 #endif
   CUDA_TRY(cudaGetLastError());
   return SPLITQ_OK;
 }
 
-template <typename T>
-int launch_k1w(const K1Params& k, int d_in, int device, cudaStream_t stream) {
+template <typename T, bool G64>
+int launch_k1w_g(const K1Params& k, int d_in, int device, cudaStream_t stream) {
   // 16-bit MAC fractions in SMEM (2 B per channel per warp): opt-in. It
   // removes the pass-G recompute but widens the MAC tie window; measured
   // 0.756 vs 0.696 ms on the 7B q-proj input, so the recompute stays default.
@@ -869,14 +869,21 @@ int launch_k1w(const K1Params& k, int d_in, int device, cudaStream_t stream) {
   const int wpr_env = wenv ? atoi(wenv) : 0;
   const bool grouped = wpr_env ? wpr_env > 1 : k.T <= 2 * sm_count(device);
   if (grouped && !smf)
-    return wpr_env >= 16 ? launch_k1w_t<T, false, 16>(k, d_in, device, stream)  // measured slower
-                         : launch_k1w_t<T, false, 8>(k, d_in, device, stream);
+    return wpr_env >= 16 ? launch_k1w_t<T, false, 16, false, G64>(k, d_in, device, stream)  // measured slower
+                         : launch_k1w_t<T, false, 8, false, G64>(k, d_in, device, stream);
   if (smf) return launch_k1w_t<T, true, 1>(k, d_in, device, stream);
   // row rounds with a CTA barrier (k1w.cuh): faster at d_in <= 8192
   const char* senv = getenv("SPLITQ_K1_SYNC");
   const bool sync = senv ? senv[0] == '1' : d_in <= 8192;
-  return sync ? launch_k1w_t<T, false, 1, true>(k, d_in, device, stream)
-              : launch_k1w_t<T, false, 1>(k, d_in, device, stream);
+  return sync ? launch_k1w_t<T, false, 1, true, G64>(k, d_in, device, stream)
+              : launch_k1w_t<T, false, 1, false, G64>(k, d_in, device, stream);
+}
+
+template <typename T>
+int launch_k1w(const K1Params& k, int d_in, int device, cudaStream_t stream) {
+  // wide aux codes (S / S_e ~ aux levels > 32): the fp64 MAC pass (k1w.cuh)
+  const bool g64 = k.use_mac && (k.aux.qmax - k.aux.qmin) > 32;
+  return g64 ? launch_k1w_g<T, true>(k, d_in, device, stream) : launch_k1w_g<T, false>(k, d_in, device, stream);
 }
 
 bool k1v3_eligible(const K1Params& k, int d_in) {
