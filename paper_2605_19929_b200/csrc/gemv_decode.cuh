@@ -106,9 +106,11 @@ __device__ __forceinline__ void gv_bar_consumers() {  // named barrier of the 8 
   asm volatile("bar.sync 1, %0;" ::"n"(GV_WARPS * 32) : "memory");
 }
 
+// The kernel body for one GEMM; bid / nbid: this CTA's index and the CTA
+// count of the GEMM (a fused launch runs two GEMMs side by side).
 template <bool PACKED, bool ASIGNED, bool LR1, int NT>
-__global__ void __launch_bounds__(GV_THREADS) gv_kernel(const __grid_constant__ GvMaps maps, const G2Params p,
-                                                        const GvArgs g, int blocks) {
+__device__ __forceinline__ void gv_body(const GvMaps& maps, const G2Params& p, const GvArgs& g, int blocks,
+                                        int bid, int nbid) {
   constexpr int RT = 8 * NT;  // staged token rows
   extern __shared__ __align__(16) uint8_t gv_smem[];
   __shared__ int s_acc[GV_WARPS][32][4];
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(GV_THREADS) gv_kernel(const __grid_constant__ 
       tma_prefetch(&maps.w);
       if (!LR1) tma_prefetch(&maps.x);
       int li = 0;
-      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+      for (int item = bid; item < items; item += nbid) {
         int u0, u1;
         unit_range(item, u0, u1);
         const int cb = item / ks_n;
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(GV_THREADS) gv_kernel(const __grid_constant__ 
   const uint8_t* arow = sact + gq * g.act_stride;  // this thread's B-operand token row
   const uint8_t* xrow = saux + gq * g.aux_stride;
   int li = 0;
-  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+  for (int item = bid; item < items; item += nbid) {
     const int cb = item / ks_n;
     int u0, u1;
     unit_range(item, u0, u1);
@@ -350,6 +352,27 @@ __global__ void __launch_bounds__(GV_THREADS) gv_kernel(const __grid_constant__ 
     }
     gv_bar_consumers();  // s_acc reused by the next item
   }
+}
+
+template <bool PACKED, bool ASIGNED, bool LR1, int NT>
+__global__ void __launch_bounds__(GV_THREADS) gv_kernel(const __grid_constant__ GvMaps maps,
+                                                        const __grid_constant__ G2Params p,
+                                                        const __grid_constant__ GvArgs g, int blocks) {
+  gv_body<PACKED, ASIGNED, LR1, NT>(maps, p, g, blocks, blockIdx.x, gridDim.x);
+}
+
+// Both low-rank first stages (CWS over the main codes, MAC over the compact
+// text-row residual codes) in one launch: CTAs [0, split) run the first,
+// the rest the second (one launch fewer on the decode chain).
+template <bool AS1, bool AS2, int NT>
+__global__ void __launch_bounds__(GV_THREADS) gv_lr1_pair_kernel(
+    const __grid_constant__ GvMaps maps1, const __grid_constant__ G2Params p1, const __grid_constant__ GvArgs g1,
+    int blocks1, const __grid_constant__ GvMaps maps2, const __grid_constant__ G2Params p2,
+    const __grid_constant__ GvArgs g2, int blocks2, int split) {
+  if ((int)blockIdx.x < split)
+    gv_body<false, AS1, true, NT>(maps1, p1, g1, blocks1, blockIdx.x, split);
+  else
+    gv_body<false, AS2, true, NT>(maps2, p2, g2, blocks2, blockIdx.x - split, gridDim.x - split);
 }
 
 }  // namespace splitq

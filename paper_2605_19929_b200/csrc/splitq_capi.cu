@@ -722,31 +722,84 @@ bool gv_fits(int64_t rows, bool packed, int64_t row_bytes, int k_aux) {
   return gv_shape(rows, packed, row_bytes, k_aux, &g, &smem);
 }
 
+// One GEMV launch, planned: tensor maps, K split, SMEM.
+struct GvPlan {
+  GvMaps maps;
+  G2Params p;
+  GvArgs g;
+  int smem;
+  int blocks;
+};
+
 // weights: [N x row_bytes] (packed 4-bit or int8 codes); aux weights b_lr [N x k_aux] fp16;
 // rows: the launch's token rows (an upper bound when p.m_count is device-side)
+int gv_plan(GvPlan& pl, const G2Params& p, const GvArgs& g, int rows, const void* w, int64_t row_bytes,
+            const __half* xb, bool packed, bool lr1, int device) {
+  pl.p = p;
+  pl.g = g;
+  const int k_aux = lr1 ? 0 : p.k_aux;
+  if (!gv_shape(rows, packed, row_bytes, k_aux, &pl.g, &pl.smem)) return fail(SPLITQ_ERR_UNSUPPORTED, "GEMV shape");
+  pl.blocks = (p.N + 15) / 16;
+  // LR1 (few channel blocks, long K): split K over CTAs so ~one CTA per SM streams
+  pl.g.ksplit = 1;
+  if (lr1 && pl.g.red)
+    pl.g.ksplit = std::max(1, std::min(pl.g.units_main, sm_count(device) / std::max(pl.blocks, 1)));
+  bool ok = make_map_2d(&pl.maps.w, w, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, p.N, row_bytes, row_bytes, 16, 128);
+  pl.maps.x = pl.maps.w;
+  if (ok && k_aux)
+    ok = make_map_2d(&pl.maps.x, xb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, p.N, k_aux, 2 * (int64_t)k_aux, 16, 64);
+  if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (GEMV)");
+  return SPLITQ_OK;
+}
+
 int launch_gv(G2Params p, GvArgs g, int rows, const void* w, int64_t row_bytes, const __half* xb, bool packed,
               bool a_signed, bool lr1, int device, cudaStream_t s) {
-  int smem;
-  const int k_aux = lr1 ? 0 : p.k_aux;
-  if (!gv_shape(rows, packed, row_bytes, k_aux, &g, &smem)) return fail(SPLITQ_ERR_UNSUPPORTED, "GEMV shape");
-  // LR1 (few channel blocks, long K): split K over CTAs so ~one CTA per SM streams
-  g.ksplit = 1;
-  if (lr1 && g.red) {
-    const int blocks = (p.N + 15) / 16;
-    g.ksplit = std::max(1, std::min(g.units_main, sm_count(device) / std::max(blocks, 1)));
+  GvPlan pl;
+  int rc = gv_plan(pl, p, g, rows, w, row_bytes, xb, packed, lr1, device);
+  if (rc) return rc;
+  const GvMaps& maps = pl.maps;
+  const int smem = pl.smem;
+  if (lr1) return a_signed ? launch_gv_n<false, true, true>(maps, pl.p, pl.g, smem, rows, device, s)
+                           : launch_gv_n<false, false, true>(maps, pl.p, pl.g, smem, rows, device, s);
+  if (packed) return a_signed ? launch_gv_n<true, true, false>(maps, pl.p, pl.g, smem, rows, device, s)
+                              : launch_gv_n<true, false, false>(maps, pl.p, pl.g, smem, rows, device, s);
+  return a_signed ? launch_gv_n<false, true, false>(maps, pl.p, pl.g, smem, rows, device, s)
+                  : launch_gv_n<false, false, false>(maps, pl.p, pl.g, smem, rows, device, s);
+}
+
+// Both LR1 GEMVs (CWS, MAC) in one launch (gv_lr1_pair_kernel)
+template <bool AS1, bool AS2, int NT>
+int launch_gv_pair_t(const GvPlan& a, const GvPlan& b, int device, cudaStream_t s) {
+  auto* kern = gv_lr1_pair_kernel<AS1, AS2, NT>;
+  static bool attr[64] = {};
+  if (device >= 0 && device < 64 && !attr[device]) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kGvSmemBudget));
+    attr[device] = true;
   }
-  GvMaps maps;
-  bool ok = make_map_2d(&maps.w, w, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, p.N, row_bytes, row_bytes, 16, 128);
-  maps.x = maps.w;
-  if (ok && k_aux)
-    ok = make_map_2d(&maps.x, xb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, p.N, k_aux, 2 * (int64_t)k_aux, 16, 64);
-  if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (GEMV)");
-  if (lr1) return a_signed ? launch_gv_n<false, true, true>(maps, p, g, smem, rows, device, s)
-                           : launch_gv_n<false, false, true>(maps, p, g, smem, rows, device, s);
-  if (packed) return a_signed ? launch_gv_n<true, true, false>(maps, p, g, smem, rows, device, s)
-                              : launch_gv_n<true, false, false>(maps, p, g, smem, rows, device, s);
-  return a_signed ? launch_gv_n<false, true, false>(maps, p, g, smem, rows, device, s)
-                  : launch_gv_n<false, false, false>(maps, p, g, smem, rows, device, s);
+  const int smem = std::max(a.smem, b.smem);
+  const int ga = a.blocks * a.g.ksplit, gb = b.blocks * b.g.ksplit;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(ga + gb));
+  cfg.blockDim = dim3(GV_THREADS);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a.maps, a.p, a.g, a.blocks, b.maps, b.p, b.g, b.blocks, ga));
+  return SPLITQ_OK;
+}
+
+int launch_gv_pair(const GvPlan& a, bool as1, const GvPlan& b, bool as2, int rows, int device, cudaStream_t s) {
+  const int nt = gv_ntiles(rows);
+#define GV_PAIR(A, B)                                                           \
+  (nt == 1 ? launch_gv_pair_t<A, B, 1>(a, b, device, s)                          \
+           : nt == 2 ? launch_gv_pair_t<A, B, 2>(a, b, device, s) : launch_gv_pair_t<A, B, 4>(a, b, device, s))
+  if (as1) return as2 ? GV_PAIR(true, true) : GV_PAIR(true, false);
+  return as2 ? GV_PAIR(false, true) : GV_PAIR(false, false);
+#undef GV_PAIR
 }
 
 // K-major int8 operand, box of box_rows rows x 128 bytes (128-B swizzle)
@@ -1035,7 +1088,8 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   // ---- low-rank first stages: fp16 columns of the auxiliary operand
   auto lr1 = [&](const void* a_codes, bool a_signed, const int8_t* bu, const float* su,
                  const int* csu, int64_t r, const float* row_s, const int* row_zp,
-                 const int* m_count, const int* row_map, int64_t col_off, int64_t lo_off) -> int {
+                 const int* m_count, const int* row_map, int64_t col_off, int64_t lo_off,
+                 GvPlan* plan = nullptr) -> int {
     GemmLaunch g{};
     const bool sw = use_swap(T);
     g.p.M = (int)T;
@@ -1066,6 +1120,7 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
       a.red = reinterpret_cast<int*>(scr) + (mac ? GV_MAX_ROWS * L->r_s : 0);
       a.cnt = reinterpret_cast<unsigned*>(scr) + GV_MAX_ROWS * (L->r_s + L->r_c) +
               (mac ? 4 * ((L->r_s + 15) / 16) : 0);
+      if (plan) return gv_plan(*plan, g.p, a, (int)T, bu, L->ld_main, nullptr, false, true, L->device);
       return launch_gv(g.p, a, (int)T, bu, L->ld_main, nullptr, false, a_signed, true, L->device, stream);
     }
     // swap-AB: the A slot (128 rows per CTA) takes the weights, B the token rows
@@ -1075,6 +1130,17 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
     if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (LR1)");
     return launch_gemm(g, L->device, T, stream, at(W.acc_scratch), W.acc_scratch_bytes);
   };
+  if (gv && L->r_s && L->r_c) {  // decode: both first stages in one launch
+    GvPlan ps, pc;
+    if ((rc = lr1(at(W.a_main), L->act.centered, L->b_us, L->s_us, L->cs_us, L->r_s,
+                  (const float*)at(W.lrs_main), L->act.centered ? nullptr : (const int*)at(W.zp_main),
+                  nullptr, nullptr, L->off_s, L->r_s8, &ps)) ||
+        (rc = lr1(at(W.a_mac), L->aux.centered, L->b_uc, L->s_uc, L->cs_uc, L->r_c,
+                  (const float*)at(W.lrs_mac), L->aux.centered ? nullptr : (const int*)at(W.zp_mac),
+                  n_text, text_rows, L->off_c, 0, &pc)) ||
+        (rc = launch_gv_pair(ps, L->act.centered, pc, L->aux.centered, (int)T, L->device, stream)))
+      return rc;
+  } else {
   if (L->r_s &&
       (rc = lr1(at(W.a_main), L->act.centered, L->b_us, L->s_us, L->cs_us, L->r_s,
                 (const float*)at(W.lrs_main), L->act.centered ? nullptr : (const int*)at(W.zp_main),
@@ -1085,6 +1151,7 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
                 (const float*)at(W.lrs_mac), L->aux.centered ? nullptr : (const int*)at(W.zp_mac),
                 n_text, text_rows, L->off_c, 0)))
     return rc;
+  }
   if (prof && (rc = prof_record(L, stream))) return rc;
 
   // ---- split GEMM: int8 main GEMM + fp16 auxiliary GEMM + merge epilogue
