@@ -646,13 +646,13 @@ int launch_gemm(GemmLaunch& g, int device, int64_t max_rows, cudaStream_t stream
 
 // Decode-sized calls (T <= gemv_max_rows()): warp-MMA GEMV kernels
 // (gemv_decode.cuh) instead of the tensor-core tiles. The kernels take up to
-// GV_MAX_ROWS = 32 rows (4 n-tiles), but measured on the 7B projections the
-// tcgen05 swap-AB path is faster from 9 rows on (batch 16: 401 vs 427 us,
-// batch 32: 411 vs 606 us per decode step), so the default cut is 8.
-// SPLITQ_GEMV_MAX_ROWS (read per call; 0 disables) overrides it.
+// GV_MAX_ROWS = 32 rows (4 n-tiles). Measured on the 7B decode step (seven
+// projections): batch 16 369 us GEMV vs 401 us tcgen05 swap-AB, batch 32
+// 501 vs 414 us, so the default cut is 16. SPLITQ_GEMV_MAX_ROWS (read per
+// call; 0 disables) overrides it.
 int gemv_max_rows() {
   const char* e = getenv("SPLITQ_GEMV_MAX_ROWS");
-  return std::min(e ? atoi(e) : 8, GV_MAX_ROWS);
+  return std::min(e ? atoi(e) : 16, GV_MAX_ROWS);
 }
 
 constexpr int kGvSmemBudget = 216 * 1024;  // dynamic; + 8 KB static partials
