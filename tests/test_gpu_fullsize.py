@@ -1,0 +1,94 @@
+"""Parity at the headline size (BASELINE config 3: one 7B projection over a
+full 65,536-token step) through size-independent properties:
+
+  * sampled rows against the oracle -- the reference is row-independent
+    (per-token parameters; MAC rows chosen by tag), so 64 sampled rows of
+    the full-size GPU result must match the oracle run on those rows alone:
+    codes and int32 main accumulators bit-exact, outputs within 1e-3 rms;
+  * chunking -- the same rows through every kernel regime (65,536-row
+    tcgen05 tiles with int8 weights, a 2000-row call on packed 4-bit
+    weights, a 16-row call on the decode GEMV kernels) give bit-identical
+    activation codes and int32 main accumulators;
+  * determinism -- two full-size runs give identical outputs.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import splitq_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+T = 65536
+
+
+@pytest.fixture(scope="module", params=["q", "down"])
+def proj(request):
+    import bench
+    import paper_2605_19929_b200 as pkg
+    from paper_2605_19929_b200 import runtime
+    dev = torch.device("cuda", 0)
+    tags, inputs, layers = bench.build_workload(pkg, T, 4, 4)
+    g, sp, layer = next(t for t in layers if t[1].name == request.param)
+    x = bench.make_input_tensor(torch, dev, T, inputs[g], tags, 77)
+    gl = runtime.GpuLayer(layer, dev)
+    return layer, gl, x, tags
+
+
+def _main_codes(gl, ws, rows, layer):
+    lay = gl.layout(rows)
+    c = ws[lay.a_main: lay.a_main + rows * lay.ld_main].view(rows, lay.ld_main)
+    return c[:, torch.from_numpy(np.asarray(layer.partition.c_main)).to(c.device)].cpu().numpy()
+
+
+def test_sampled_rows_match_oracle(proj):
+    layer, gl, x, tags = proj
+    dev = x.device
+    td = torch.from_numpy(tags).to(dev)
+    raw = gl.run(x, td, raw=True)
+    y = gl.run(x, td).double()
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(3)
+    rows = np.sort(rng.choice(T, 64, replace=False))
+    xs = x[torch.from_numpy(rows).to(dev)].double().cpu().numpy()
+    ts = tags[rows]
+    L = orc.from_reference_layer(layer)
+    acc = orc.accumulators(L, xs, ts)
+    act = orc.activation_codes(L, xs, ts)
+    w = orc.weight_codes(L)
+    lay = gl.layout(T)
+    main = acc["main"] if lay.code_centered_main else \
+        acc["main"] + act["main"][2][:, None] * w["main"][0].sum(axis=0)[None, :]
+    np.testing.assert_array_equal(raw[0][torch.from_numpy(rows).to(dev)].cpu().numpy().astype(np.int64), main)
+    ref = orc.forward(L, xs, ts)
+    got = y[torch.from_numpy(rows).to(dev)].cpu().numpy()
+    rms = np.sqrt(np.mean(ref ** 2))
+    # fp16 output storage: one rounding (2^-11 relative) on top of the bar
+    excess = np.abs(got - ref) - 2.0 ** -11 * np.abs(ref)
+    assert np.max(excess) <= 1e-3 * rms
+
+
+def test_chunks_through_every_regime_bit_identical(proj):
+    layer, gl, x, tags = proj
+    dev = x.device
+    td = torch.from_numpy(tags).to(dev)
+    ws_full = gl.workspace(T).clone()  # keep the full run's workspace
+    raw = gl.run(x, td, raw=True, ws=ws_full)
+    torch.cuda.synchronize()
+    codes_full = _main_codes(gl, ws_full, T, layer)
+    for r0, n in ((1000, 2000), (40000, 16), (T - 8, 8)):
+        ws = torch.empty(int(gl.layout(n).total_bytes), dtype=torch.uint8, device=dev)
+        part = gl.run(x[r0:r0 + n].contiguous(), td[r0:r0 + n].contiguous(), raw=True, ws=ws)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(part[0].cpu().numpy(), raw[0][r0:r0 + n].cpu().numpy())
+        np.testing.assert_array_equal(_main_codes(gl, ws, n, layer), codes_full[r0:r0 + n])
+
+
+def test_full_size_deterministic(proj):
+    layer, gl, x, tags = proj
+    td = torch.from_numpy(tags).to(x.device)
+    a = gl.run(x, td, out_dtype=torch.float16)
+    b = gl.run(x, td, out_dtype=torch.float16)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
