@@ -26,7 +26,8 @@ from .layer_io import (
     save_tensor,
 )
 from .lowrank import LowRankBranch, SvdFactors, build_branch, default_rank, truncated_svd
-from .mocd import ChannelPartition, MocdConfig, select_topk, trivial_partition
+from .mocd import ChannelPartition, MocdConfig, jaccard, outlier_set, select_topk, trivial_partition
+from .calibrate import stability_report
 from .quantizer import (
     Granularity,
     QuantParams,

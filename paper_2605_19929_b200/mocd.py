@@ -72,3 +72,15 @@ def select_topk(scores, k: int) -> np.ndarray:  # mocd.py:80-89
         return np.empty(0, dtype=np.int64)
     order = np.argsort(-scores, kind="stable")
     return np.sort(order[:k]).astype(np.int64)
+
+
+def jaccard(a, b) -> float:  # mocd.py:182-190
+    """|A n B| / |A u B|; two empty sets count as identical (1.0)."""
+    sa = set(np.asarray(a, dtype=np.int64).tolist())
+    sb = set(np.asarray(b, dtype=np.int64).tolist())
+    union = sa | sb
+    return 1.0 if not union else len(sa & sb) / len(union)
+
+
+def outlier_set(partition) -> np.ndarray:  # calibrate.py:297-298
+    return np.sort(np.concatenate([partition.c_text, partition.c_vision]))

@@ -198,7 +198,22 @@ def gen_layer_dir():
     print("wrote", d, sorted(os.listdir(d)))
 
 
+def gen_stability():
+    """The reference's stability_report (calibrate.py:301-329) on a small
+    planted batch: subset sizes, trials, the Jaccard mean / std per size."""
+    from modquant.calibrate import stability_report
+    batch = generate(SynthConfig(tokens_text=180, tokens_vision=120, dim=64, vision_outlier_channels=(2, 9),
+                                 text_outlier_channels=(17, 40), vision_outlier_scale=1.6,
+                                 text_instability=0.15, seed=5))
+    cfg = mocd.MocdConfig(ratio_vision=4 / 64, ratio_text=4 / 64)
+    sizes, ref_size, trials = [30, 90, 200], 260, 4
+    rep = stability_report(batch, cfg, sizes, ref_size, trials, seed=2)
+    save("stability.npz", x=batch.data, tags=batch.tags, sizes=np.array(sizes), ref_size=np.array(ref_size),
+         trials=np.array(trials), ratios=np.array([cfg.ratio_vision, cfg.ratio_text]),
+         mean=np.array([r["mean_jaccard"] for r in rep]), std=np.array([r["std_jaccard"] for r in rep]))
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["quantizer", "layers", "config1", "mocd", "layer_dir"]
+    which = sys.argv[1:] or ["quantizer", "layers", "config1", "mocd", "layer_dir", "stability"]
     for name in which:
         globals()["gen_" + name]()

@@ -88,3 +88,18 @@ def test_errors():
         mg.build_partition(b, pkg.MocdConfig(ratio_vision=0.25, ratio_text=0.0))
     with pytest.raises(ValueError, match="vision"):
         mg.vision_score(b)
+
+
+def test_stability_report_matches_reference():
+    """calibrate.stability_report on the device against the reference's own
+    report (tests/golden/stability.npz, gen_golden.py gen_stability)."""
+    import os
+    pkg, _ = _pkg()
+    d = np.load(os.path.join(os.path.dirname(__file__), "golden", "stability.npz"))
+    cfg = pkg.MocdConfig(float(d["ratios"][0]), float(d["ratios"][1]))
+    batch = pkg.ActivationBatch(torch.from_numpy(d["x"]).cuda(), torch.from_numpy(d["tags"]).cuda())
+    rep = pkg.stability_report(batch, cfg, [int(s) for s in d["sizes"]], int(d["ref_size"]),
+                               int(d["trials"]), seed=2)
+    np.testing.assert_array_equal([r["mean_jaccard"] for r in rep], d["mean"])
+    np.testing.assert_array_equal([r["std_jaccard"] for r in rep], d["std"])
+    assert [r["subset_size"] for r in rep] == [int(s) for s in d["sizes"]]
