@@ -731,12 +731,13 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
 
     KW_STAMP(4)
     // ------------------------------------------------ outlier codes + aux segments
-    if (p.n_text > 0 && wl % WPR == 0)
+    // (a row group spreads both outlier paths over all its threads)
+    if (p.n_text > 0)
       outlier_codes(p, row, xr, p.c_text, p.d_text, p.n_text, p.ld_text, p.a_text, rt,
-                    rt.S * rrho, p.lr_off_t, p.kt16);
-    if (p.n_vis > 0 && wl % WPR == (WPR > 1 ? 1 : 0))
+                    rt.S * rrho, p.lr_off_t, p.kt16, WPR > 1 ? gl : -1, GT);
+    if (p.n_vis > 0)
       outlier_codes(p, row, xr, p.c_vis, p.d_vis, p.n_vis, p.ld_vis, p.a_vis, rv, rv.S * rrho,
-                    p.lr_off_v, p.kv16);
+                    p.lr_off_v, p.kv16, WPR > 1 ? gl : -1, GT);
     if (p.k_lr > 0) {  // the low-rank columns of the aux operand row: LR1 fills them
       uint4* lr = reinterpret_cast<uint4*>(p.lr_a + (int64_t)row * p.k_lr + p.lr_off_s);
       for (int i = gl; i < (p.k_lr - p.lr_off_s) / 8; i += GT) lr[i] = make_uint4(0, 0, 0, 0);

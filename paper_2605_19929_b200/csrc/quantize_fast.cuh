@@ -454,12 +454,11 @@ __device__ void outlier_params(const K1Params& p, const T* xs, const int* cols, 
 template <typename T>
 __device__ void outlier_codes(const K1Params& p, int row, const T* xs, const int* cols,
                               const double* d, int n, int ld, int8_t* codes, const RowParams& rp,
-                              double fac, int seg_off, int k16) {
-  const int lane = threadIdx.x & 31;
+                              double fac, int seg_off, int k16, int k0 = -1, int step = 32) {
   int8_t* out = codes + (int64_t)row * ld;
   __half* seg = p.k_lr > 0 ? p.lr_a + (int64_t)row * p.k_lr + seg_off : nullptr;
   const int lim = max(ld, k16);
-  for (int k = lane; k < lim; k += 32) {
+  for (int k = k0 < 0 ? (int)(threadIdx.x & 31) : k0; k < lim; k += step) {
     int c = 0;
     double a = 0.0;
     if (k < n) {
