@@ -405,17 +405,22 @@ __device__ __forceinline__ KwConsts kw_consts2(double lo, double hi, double S, d
   const double vmax = fmax(fabs(vl), fabs(vh));
   const double err = vmax * 4.76837158203125e-07 + err_extra;  // 2^-21
   c.safe = vmax < 1048576.0;
-  int k = 10;
-  while (k < 22 && !((double)(1 << (k - 1)) > vmax + 2.0)) ++k;
-  const double ulp = ldexp(1.0, k - 23);
+  // k: the smallest k in [10, 22] with 2^(k-1) > vmax + 2, from the exponent
+  // of vmax + 2 (2^e <= vmax + 2 < 2^(e+1) -> k = e + 2); powers of two by
+  // their bit patterns (no loop, no ldexp / division on the row's critical path)
+  const double vm2 = vmax + 2.0;
+  int k = 22;
+  if (vm2 < 4194304.0) k = min(22, max(10, ((__double2hiint(vm2) >> 20) & 0x7FF) - 1023 + 2));
+  const double ulp = __hiloint2double((k - 23 + 1023) << 20, 0);
+  const double rulp = __hiloint2double((23 - k + 1023) << 20, 0);
   c.F = (uint32_t)(23 - k);
   c.fm = (1u << c.F) - 1u;
-  const double Wd = floor((err + 0.5 * ulp) / ulp) + 1.0;
+  const double Wd = floor((err + 0.5 * ulp) * rulp) + 1.0;  // exact: rulp = 1 / ulp is a power of two
   if (!(Wd < (double)(1 << (c.F - 2)))) c.safe = 0;
   const double W = c.safe ? Wd : 1.0;
   c.W2 = (uint32_t)(2.0 * W);
   const int zq = s.centered ? 0 : zp;
-  const double b = 1.5 * ldexp(1.0, k) + (double)zq;
+  const double b = 1.5 * __hiloint2double((k + 1023) << 20, 0) + (double)zq;
   c.rs = (float)rS;
   c.base = (float)b;
   c.C = (float)(b + 0.5 + W * ulp);
