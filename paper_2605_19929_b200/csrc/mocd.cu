@@ -487,11 +487,17 @@ __device__ void ts_pairwise_pass(const uint16_t* col, int n, int nk, double nc, 
 __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
     const uint16_t* counts_t, int64_t ld, int n_cand, int n_text, int k_req, int max_iter, int c0,
     int c1, double* scores) {
+  // SMEM: a bitmask of the levels present, then one region used twice: the
+  // (cumulative) level histogram while the centres are initialised, then the
+  // level -> cluster map, the segment counts and the subtree sums. The peak
+  // is the histogram alone, so D = 18944 fits two CTAs per SM.
   extern __shared__ __align__(16) uint8_t ts_smem[];
-  double* val = reinterpret_cast<double*>(ts_smem);                        // [TS_THREADS]
-  int* hist = reinterpret_cast<int*>(val + TS_THREADS);                    // [n_cand + 1] -> cumulative
-  int* seg = hist + (n_cand + 1);                                          // [TS_THREADS x TS_KMAX]
-  int8_t* asg = reinterpret_cast<int8_t*>(seg + TS_THREADS * TS_KMAX);     // [n_cand + 1] level -> cluster
+  uint32_t* present = reinterpret_cast<uint32_t*>(ts_smem);               // [(n_cand + 32) / 32]
+  uint8_t* region = ts_smem + (((n_cand + 32) / 32 * 4 + 15) & ~15);
+  int* hist = reinterpret_cast<int*>(region);                              // [n_cand + 1] -> cumulative
+  double* val = reinterpret_cast<double*>(region);                         // [TS_THREADS]        (after)
+  int* seg = reinterpret_cast<int*>(val + TS_THREADS);                     // [TS_THREADS x KMAX] (after)
+  int8_t* asg = reinterpret_cast<int8_t*>(seg + TS_THREADS * TS_KMAX);     // [n_cand + 1]        (after)
   __shared__ TsShared sh;
   __shared__ double centers[TS_KMAX], new_centers[TS_KMAX];
   __shared__ int distinct, changed;
@@ -506,13 +512,17 @@ __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
     sh.val = val;
   }
 
-  for (int v = tid; v <= n_cand; v += TS_THREADS) hist[v] = 0, asg[v] = 0;
+  for (int v = tid; v <= n_cand; v += TS_THREADS) hist[v] = 0;
+  for (int w = tid; w < (n_cand + 32) / 32; w += TS_THREADS) present[w] = 0;
   if (tid == 0) distinct = 0;
   __syncthreads();
   for (int i = tid; i < n_text; i += TS_THREADS) atomicAdd(&hist[col[i]], 1);
   __syncthreads();
   for (int v = tid; v <= n_cand; v += TS_THREADS)
-    if (hist[v]) atomicAdd(&distinct, 1);
+    if (hist[v]) {
+      atomicAdd(&distinct, 1);
+      atomicOr(&present[v >> 5], 1u << (v & 31));
+    }
   __syncthreads();
   // cumulative histogram (one thread; n_cand <= ~20k)
   if (tid == 0) {
@@ -525,8 +535,16 @@ __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
   __syncthreads();
   const int k = min(k_req, distinct);
   const int n = n_text;
+  // from here on the region holds asg / seg / val (the histogram is only
+  // read by the centre initialisation, before the switch below)
+  auto release_hist = [&]() {
+    __syncthreads();
+    for (int v = tid; v <= n_cand; v += TS_THREADS) asg[v] = 0;
+    __syncthreads();
+  };
 
   if (k <= 1) {
+    release_hist();
     // np.var(values): mean = sum / n, then mean((v - mean)^2) (pairwise sums)
     ts_pairwise_pass<2>(col, n, 1, nc, asg, centers, sh, vec);
     if (tid == 0) centers[0] = sh.tot[0] / (double)n;
@@ -561,11 +579,11 @@ __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
     const double diff = b - a;
     centers[tid] = t >= 0.5 ? b - diff * (1.0 - t) : a + diff * t;
   }
-  __syncthreads();
+  release_hist();
   // level assignment: argmin |v - c_j|, ties to the lower index (np.argmin)
   auto assign_levels = [&](const double* cen, bool track) {
     for (int v = tid; v <= n_cand; v += TS_THREADS) {
-      if (hist[v] - (v ? hist[v - 1] : 0) == 0) continue;
+      if (!((present[v >> 5] >> (v & 31)) & 1u)) continue;
       const double x = (double)v / nc;
       int best = 0;
       double bd = fabs(x - cen[0]);
@@ -731,7 +749,9 @@ int splitq_mocd_text_score(const uint16_t* counts_t, int64_t ld, int64_t n_cand,
   if (k > n_text) return mfail(SPLITQ_ERR_INVALID, "cluster count exceeds number of text tokens");
   if (k > TS_KMAX) return mfail(SPLITQ_ERR_UNSUPPORTED, "at most 8 clusters on the GPU path");
   if (c1 <= c0) return SPLITQ_OK;
-  const size_t smem = (size_t)TS_THREADS * 8 + (size_t)(n_cand + 1) * 5 + (size_t)TS_THREADS * TS_KMAX * 4 + 16;
+  const size_t bits = (size_t)(((n_cand + 32) / 32 * 4 + 15) & ~15);
+  const size_t after = (size_t)TS_THREADS * 8 + (size_t)TS_THREADS * TS_KMAX * 4 + (size_t)(n_cand + 1);
+  const size_t smem = bits + std::max((size_t)(n_cand + 1) * 4, after) + 16;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(mocd_text_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
