@@ -92,3 +92,29 @@ def test_full_size_deterministic(proj):
     b = gl.run(x, td, out_dtype=torch.float16)
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+
+
+def test_bf16_sampled_rows_match_oracle():
+    """The bf16 input path at the headline size (q-proj, 65,536 tokens)."""
+    import bench
+    import paper_2605_19929_b200 as pkg
+    from paper_2605_19929_b200 import runtime
+    dev = torch.device("cuda", 0)
+    tags, inputs, layers = bench.build_workload(pkg, T, 4, 4)
+    g, sp, layer = next(t for t in layers if t[1].name == "q")
+    x = bench.make_input_tensor(torch, dev, T, inputs[g], tags, 91).to(torch.bfloat16)
+    gl = runtime.GpuLayer(layer, dev)
+    td = torch.from_numpy(tags).to(dev)
+    raw = gl.run(x, td, raw=True)
+    torch.cuda.synchronize()
+    rows = np.sort(np.random.default_rng(5).choice(T, 64, replace=False))
+    ridx = torch.from_numpy(rows).to(dev)
+    xs = x[ridx].double().cpu().numpy()
+    ts = tags[rows]
+    L = orc.from_reference_layer(layer)
+    acc = orc.accumulators(L, xs, ts)
+    act = orc.activation_codes(L, xs, ts)
+    w = orc.weight_codes(L)
+    main = acc["main"] if gl.layout(T).code_centered_main else \
+        acc["main"] + act["main"][2][:, None] * w["main"][0].sum(axis=0)[None, :]
+    np.testing.assert_array_equal(raw[0][ridx].cpu().numpy().astype(np.int64), main)
