@@ -231,6 +231,21 @@ __device__ __forceinline__ void gv_body(const GvMaps& maps, const G2Params& p, c
     const int cb = item / ks_n;
     int u0, u1;
     unit_range(item, u0, u1);
+    // the block's column constants (channels cb*16 + gq and + 8), loaded now
+    // so their latency hides under the MMA units (warp 0 runs the epilogue)
+    float c_s[2] = {0.f, 0.f}, c_k[2] = {0.f, 0.f};
+    int c_cs[2] = {0, 0};
+    if (warp == 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = cb * 16 + gq + 8 * h;
+        if (col < p.N) {
+          c_s[h] = p.col_s[col];
+          if (p.row_zp) c_cs[h] = p.col_cs[col];
+          if (!LR1 && p.k_aux > 0 && p.mode != G2_RAW) c_k[h] = p.col_kappa[col];
+        }
+      }
+    }
     int acc[NT][4];
     float ax[NT][4];
 #pragma unroll
@@ -330,10 +345,10 @@ __device__ __forceinline__ void gv_body(const GvMaps& maps, const G2Params& p, c
       for (int e = 0; e < 4; ++e) {
         const int col = cb * 16 + gq + 8 * (e >> 1), tk = e & 1, t = 8 * j + 2 * tig + tk;
         if (!last || col >= p.N || t >= M) continue;
-        const int acc_c = sa[e] - (p.row_zp ? t_zp[j][tk] * p.col_cs[col] : 0);
+        const int acc_c = sa[e] - (p.row_zp ? t_zp[j][tk] * c_cs[e >> 1] : 0);
         if (LR1) {
           __half* o = reinterpret_cast<__half*>(p.out);
-          const float v = acc_c == 0 ? 0.f : t_s[j][tk] * p.col_s[col] * (float)acc_c;
+          const float v = acc_c == 0 ? 0.f : t_s[j][tk] * c_s[e >> 1] * (float)acc_c;
           if (!(fabsf(v) <= 65504.f) && p.err) atomicOr(p.err, 8 /*ERR_LR_RANGE*/);
           const __half hv = __float2half_rn(v);
           o[(int64_t)t_orow[j][tk] * p.ldo + p.col_off + col] = hv;
@@ -344,8 +359,8 @@ __device__ __forceinline__ void gv_body(const GvMaps& maps, const G2Params& p, c
           reinterpret_cast<int*>(p.out)[idx] = sa[e];
           if (p.k_aux && p.raw_aux) p.raw_aux[idx] = sx[e];
         } else {
-          float v = t_s[j][tk] * p.col_s[col] * (float)acc_c;
-          if (p.k_aux > 0) v = fmaf(t_rho[j][tk] * p.col_kappa[col], sx[e], v);
+          float v = t_s[j][tk] * c_s[e >> 1] * (float)acc_c;
+          if (p.k_aux > 0) v = fmaf(t_rho[j][tk] * c_k[e >> 1], sx[e], v);
           g2_store1(p, (int64_t)t * p.ldo + col, v);
         }
       }
