@@ -920,7 +920,13 @@ int launch_k1w_g(const K1Params& k, int d_in, int device, cudaStream_t stream) {
   // save). SPLITQ_K1_WPR=1|8|16 overrides.
   const char* wenv = getenv("SPLITQ_K1_WPR");  // read per call: tests switch it
   const int wpr_env = wenv ? atoi(wenv) : 0;
-  const bool grouped = wpr_env ? wpr_env > 1 : k.T <= 2 * sm_count(device);
+  // row groups also for wide rows (d_in > 8192) when the warp-per-row launch
+  // would give each warp at most one row: one warp's serial passes over a
+  // wide row are then the critical path (3B down, d_in 11008, 4096 rows:
+  // 343 -> 147 us); from ~2 rows per warp on, warp rows win (7B down at
+  // 8192 rows: 789 vs 980 us)
+  const bool grouped = wpr_env ? wpr_env > 1
+                               : k.T <= 2 * sm_count(device) || (d_in > 8192 && k.T <= 32 * sm_count(device));
   if (grouped && !smf)
     return wpr_env >= 16 ? launch_k1w_t<T, false, 16, false, G64>(k, d_in, device, stream)  // measured slower
                          : launch_k1w_t<T, false, 8, false, G64>(k, d_in, device, stream);
