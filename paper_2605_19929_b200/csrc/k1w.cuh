@@ -201,6 +201,31 @@ __device__ __forceinline__ void kw_load(const K1Params& p, const uint4* xg, int 
   d[4] = db.x; d[5] = db.y; d[6] = db.z; d[7] = db.w;
 }
 
+// one chunk's raw operands, loaded a loop iteration ahead (PF)
+struct KwRaw {
+  uint4 w;
+  float4 da, db;
+};
+__device__ __forceinline__ KwRaw kw_ldraw(const K1Params& p, const uint4* xg, int j) {
+  KwRaw r;
+  r.w = kw_ldg(xg + j);
+  r.da = __ldg(reinterpret_cast<const float4*>(p.d_main32) + 2 * j);
+  r.db = __ldg(reinterpret_cast<const float4*>(p.d_main32) + 2 * j + 1);
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ void kw_cvt(const KwRaw& r, float (&x)[8], float (&d)[8]) {
+  const uint32_t ws[4] = {r.w.x, r.w.y, r.w.z, r.w.w};
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const float2 f2 = XW<T>::to_f2(ws[h]);
+    x[2 * h] = f2.x;
+    x[2 * h + 1] = f2.y;
+  }
+  d[0] = r.da.x; d[1] = r.da.y; d[2] = r.da.z; d[3] = r.da.w;
+  d[4] = r.db.x; d[5] = r.db.y; d[6] = r.db.z; d[7] = r.db.w;
+}
+
 // the same from the row group's SMEM copy (x plane + two d planes)
 template <typename T>
 __device__ __forceinline__ void kw_load_s(const uint4* xs, const float4* ds, int nch, int j,
@@ -494,7 +519,10 @@ struct KwZ {
 // chunks strided over all WPR x 32 threads; warp reductions are completed
 // across the group through SMEM (kw_gmin), the per-row parameters are
 // computed redundantly by every warp (deterministic) and stored by warp 0.
-template <typename T, bool SMF, int WPR, bool SYNC = false, bool G64 = false>
+// PF (warp rows only): each pass issues the next chunk's loads one iteration
+// ahead. For few rows per warp on wide rows, where a warp's serial passes
+// are the critical path; it costs registers (occupancy) at full load.
+template <typename T, bool SMF, int WPR, bool SYNC = false, bool G64 = false, bool PF = false>
 __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : KW_THREADS)
     k1w_kernel(const K1Params p, int d_in) {
   static_assert(!(SMF && WPR > 1), "SMEM MAC fractions are per-warp rows");
@@ -552,10 +580,19 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
     kw_ext_init(elo);
     kw_ext_init(ehi);
     uint32_t nm = 0u;
+    KwRaw pa{};
+    if (PF && gl < nchunks) pa = kw_ldraw(p, xg, gl);
     for (int j = gl; j < nchunks; j += GT) {
-      const uint4 w = kw_ldg(xg + j);
-      const float4 da = __ldg(reinterpret_cast<const float4*>(p.d_main32) + 2 * j);
-      const float4 db = __ldg(reinterpret_cast<const float4*>(p.d_main32) + 2 * j + 1);
+      uint4 w;
+      float4 da, db;
+      if constexpr (PF) {
+        w = pa.w, da = pa.da, db = pa.db;
+        if (j + GT < nchunks) pa = kw_ldraw(p, xg, j + GT);
+      } else {
+        w = kw_ldg(xg + j);
+        da = __ldg(reinterpret_cast<const float4*>(p.d_main32) + 2 * j);
+        db = __ldg(reinterpret_cast<const float4*>(p.d_main32) + 2 * j + 1);
+      }
       if constexpr (WPR > 1) {
         xs[j] = w;
         ds[j] = da;
@@ -757,13 +794,18 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
     kw_ext_init(fhi);
     int qn = 0;
     if (c.safe) {
+      KwRaw pe{};
+      if (PF && gl < nchunks) pe = kw_ldraw(p, xg, gl);
       for (int j0 = 0; j0 < nchunks; j0 += GT) {
         const int j = j0 + gl;
         bool flag = false;
+        KwRaw cur = pe;
+        if (PF && j + GT < nchunks) pe = kw_ldraw(p, xg, j + GT);
         if (j < nchunks) {
           float z[8], v[8], x[8], d[8];
           uint32_t b[8];
-          kwl(j, x, d);
+          if constexpr (PF) kw_cvt<T>(cur, x, d);
+          else kwl(j, x, d);
           kw_mulz(x, d, z);
           kw_vt(z, c, v, b);
           *reinterpret_cast<uint2*>(arow + 8 * j) = kw_pack_shift(b, c.F);
@@ -957,9 +999,14 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
         kw_enqueue(q, qn, flag, j);
       }
     } else if (!allg) {
+      constexpr bool PG = PF && !SMF;
+      KwRaw pg{};
+      if (PG && gl < nchunks) pg = kw_ldraw(p, xg, gl);
       for (int j0 = 0; j0 < nchunks; j0 += GT) {
         const int j = j0 + gl;
         bool flag = false;
+        KwRaw cur = pg;
+        if (PG && j + GT < nchunks) pg = kw_ldraw(p, xg, j + GT);
         if (j < nchunks) {
           uint32_t be[8];
           bool mflag = false;
@@ -979,7 +1026,8 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
           } else {
             float f[8], x[8], d[8], z[8], v[8];
             uint32_t b[8];
-            kwl(j, x, d);
+            if constexpr (PG) kw_cvt<T>(cur, x, d);
+            else kwl(j, x, d);
             kw_mulz(x, d, z);
             kw_vt(z, c, v, b);
             kw_frac(v, b, c, f);

@@ -872,18 +872,18 @@ int launch_k1_dt(const K1Params& k, int d_in, cudaStream_t s) {
 // fp32 fast path with certified exact fp64 fallback (k1w.cuh).
 unsigned long long* k1w_trace_last = nullptr;
 
-template <typename T, bool SMF, int WPR, bool SYNC = false, bool G64 = false>
+template <typename T, bool SMF, int WPR, bool SYNC = false, bool G64 = false, bool PF = false>
 int launch_k1w_t(const K1Params& k, int d_in, int device, cudaStream_t stream) {
   const int threads = WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : KW_THREADS;
   const size_t smem = k1w_smem(d_in, threads / 32, SMF, WPR);
   static int attr_dev[64] = {0};
   if (device >= 0 && device < 64 && !attr_dev[device]) {
-    CUDA_TRY(cudaFuncSetAttribute(k1w_kernel<T, SMF, WPR, SYNC, G64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_TRY(cudaFuncSetAttribute(k1w_kernel<T, SMF, WPR, SYNC, G64, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   200 * 1024));
     attr_dev[device] = 1;
   }
   int per_sm = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1w_kernel<T, SMF, WPR, SYNC, G64>, threads, smem));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1w_kernel<T, SMF, WPR, SYNC, G64, PF>, threads, smem));
   if (per_sm < 1) return SPLITQ_ERR_UNSUPPORTED;
   int64_t grid;
   if (WPR > 1) {  // one row per CTA
@@ -899,9 +899,9 @@ int launch_k1w_t(const K1Params& k, int d_in, int device, cudaStream_t stream) {
   K1Params kt = k;
   kt.trace = kw_trace_buf;
   k1w_trace_last = kw_trace_buf;
-  k1w_kernel<T, SMF, WPR, SYNC, G64><<<(unsigned)grid, threads, smem, stream>>>(kt, d_in);
+  k1w_kernel<T, SMF, WPR, SYNC, G64, PF><<<(unsigned)grid, threads, smem, stream>>>(kt, d_in);
 #else
-  k1w_kernel<T, SMF, WPR, SYNC, G64><<<(unsigned)grid, threads, smem, stream>>>(k, d_in);
+  k1w_kernel<T, SMF, WPR, SYNC, G64, PF><<<(unsigned)grid, threads, smem, stream>>>(k, d_in);
 #endif
   CUDA_TRY(cudaGetLastError());
   return SPLITQ_OK;
@@ -934,8 +934,12 @@ int launch_k1w_g(const K1Params& k, int d_in, int device, cudaStream_t stream) {
   // row rounds with a CTA barrier (k1w.cuh): faster at d_in <= 8192
   const char* senv = getenv("SPLITQ_K1_SYNC");
   const bool sync = senv ? senv[0] == '1' : d_in <= 8192;
-  return sync ? launch_k1w_t<T, false, 1, true, G64>(k, d_in, device, stream)
-              : launch_k1w_t<T, false, 1, false, G64>(k, d_in, device, stream);
+  if (sync) return launch_k1w_t<T, false, 1, true, G64>(k, d_in, device, stream);
+  // wide rows with a few rows per warp: loads one chunk ahead (k1w.cuh PF)
+  const char* penv = getenv("SPLITQ_K1_PF");
+  const bool pf = penv ? penv[0] == '1' : k.T <= 128 * sm_count(device);
+  return pf ? launch_k1w_t<T, false, 1, false, G64, true>(k, d_in, device, stream)
+            : launch_k1w_t<T, false, 1, false, G64>(k, d_in, device, stream);
 }
 
 template <typename T>

@@ -119,14 +119,17 @@ SHAPES = {
 }
 
 
-@pytest.fixture(params=[("1", "0"), ("1", "1"), ("8", "0"), ("16", "0")],
-                ids=["warp_rows", "warp_rows_sync", "cta8_rows", "cta16_rows"], autouse=True)
+@pytest.fixture(params=[("1", "0", "0"), ("1", "0", "1"), ("1", "1", "0"), ("8", "0", "0"), ("16", "0", "0")],
+                ids=["warp_rows", "warp_rows_prefetch", "warp_rows_sync", "cta8_rows", "cta16_rows"],
+                autouse=True)
 def k1_row_group(request, monkeypatch):
-    """Every case runs with one warp per row (prefill; with and without the
-    per-round CTA barrier) and with 8- / 16-warp row groups (decode-sized
-    calls); the library reads SPLITQ_K1_WPR / SPLITQ_K1_SYNC per call."""
+    """Every case runs with one warp per row (prefill; plain, with loads one
+    chunk ahead, with the per-round CTA barrier) and with 8- / 16-warp row
+    groups (decode-sized calls); the library reads SPLITQ_K1_WPR / _SYNC /
+    _PF per call."""
     monkeypatch.setenv("SPLITQ_K1_WPR", request.param[0])
     monkeypatch.setenv("SPLITQ_K1_SYNC", request.param[1])
+    monkeypatch.setenv("SPLITQ_K1_PF", request.param[2])
 
 
 @pytest.mark.parametrize("dt", DTS, ids=["f16", "bf16"])
