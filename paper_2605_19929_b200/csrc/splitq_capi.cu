@@ -613,10 +613,14 @@ int launch_gemm(GemmLaunch& g, int device, int64_t max_rows, cudaStream_t stream
 #ifdef G2_TRACE
   static unsigned long long* trace_buf = nullptr;
   if (!trace_buf) cudaMalloc(&trace_buf, 148 * 8 * 8);
-  cudaMemsetAsync(trace_buf, 0, 148 * 8 * 8, stream);
-  g.p.trace = trace_buf;
-  g2_trace_last = trace_buf;
-  g2_trace_ctas = 2 * pairs;
+  // SPLITQ_TRACE_MODE=<G2 mode number>: trace only launches of that mode
+  const char* tm = getenv("SPLITQ_TRACE_MODE");
+  if (!tm || atoi(tm) == g.p.mode) {
+    cudaMemsetAsync(trace_buf, 0, 148 * 8 * 8, stream);
+    g.p.trace = trace_buf;
+    g2_trace_last = trace_buf;
+    g2_trace_ctas = 2 * pairs;
+  }
 #endif
   // programmatic dependent launch (set-up and first weight loads overlap the
   // preceding kernel's tail; see the kernel head)
