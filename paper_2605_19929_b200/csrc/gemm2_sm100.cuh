@@ -628,11 +628,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
       }
       const uint32_t lane_base = tmem + ((uint32_t)(lq * 32) << 16) + b * p.bn;
       const uint32_t lane_aux = tmem + ((uint32_t)(lq * 32) << 16) + 2 * p.bn;
+      const int orow = row_ok && p.row_map ? p.row_map[row] : row;  // LR1 destination row
       for (int c0 = 0; c0 < p.bn; c0 += 32) {
         uint32_t am[32], af[32];
         tmem_ld32(lane_base + c0, am);
         if (has_aux) tmem_ld32(lane_aux + c0, af);
         tmem_wait_ld();
+        if (p.mode == G2_LR1) {
+          // the chunk's 32 column constants: one load per lane, broadcast by
+          // shuffles (all lanes take part; rows past M only skip the stores)
+          const int cl = n0 + c0 + lane;
+          const float sw_l = cl < p.N ? p.col_s[cl] : 0.f;
+          const int cs_l = cl < p.N && p.row_zp ? p.col_cs[cl] : 0;
+          __half* o = reinterpret_cast<__half*>(p.out) + (int64_t)orow * p.ldo + p.col_off;
+          const bool vec = ((p.ldo | p.col_off | p.lo_off) & 7) == 0;
+#pragma unroll
+          for (int g = 0; g < 32; g += 8) {
+            const int colg = n0 + c0 + g;
+            __half hv[8], lv[8];
+            bool bad = false;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float sw = __shfl_sync(0xffffffffu, sw_l, g + j);
+              const int cs = __shfl_sync(0xffffffffu, cs_l, g + j);
+              const int acc = (int)am[g + j] - zp * cs;
+              const float v = acc == 0 ? 0.f : s_row * sw * (float)acc;
+              bad |= row_ok && colg + j < p.N && !(fabsf(v) <= 65504.f);
+              hv[j] = __float2half_rn(v);
+              lv[j] = __float2half_rn(v - __half2float(hv[j]));
+            }
+            if (bad && p.err) atomicOr(p.err, 8 /*ERR_LR_RANGE*/);
+            if (!row_ok) continue;
+            if (vec && colg + 8 <= p.N) {  // 8 columns -> one 16-byte store (+ one for lo)
+              *reinterpret_cast<uint4*>(o + colg) = *reinterpret_cast<const uint4*>(hv);
+              if (p.lo_off) *reinterpret_cast<uint4*>(o + p.lo_off + colg) = *reinterpret_cast<const uint4*>(lv);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (colg + j < p.N) {
+                  o[colg + j] = hv[j];
+                  if (p.lo_off) o[p.lo_off + colg + j] = lv[j];
+                }
+            }
+          }
+          continue;
+        }
         if (!row_ok) continue;
         if (p.mode == G2_ACC) {
           const int64_t so = (int64_t)(item % ksplit) * p.acc_slice;
@@ -654,32 +694,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
               const int64_t idx = (int64_t)row * p.ldo + col;
               o[idx] = (int)am[j];
               if (has_aux && p.raw_aux) p.raw_aux[idx] = __uint_as_float(af[j]);
-            }
-          }
-        } else if (p.mode == G2_LR1) {
-          const int orow = p.row_map ? p.row_map[row] : row;
-          __half* o = reinterpret_cast<__half*>(p.out) + (int64_t)orow * p.ldo + p.col_off;
-          const bool vec = ((p.ldo | p.col_off | p.lo_off) & 7) == 0;
-#pragma unroll
-          for (int g = 0; g < 32; g += 8) {
-            const int colg = n0 + c0 + g;
-            if (vec && colg + 8 <= p.N) {  // 8 columns -> one 16-byte store (+ one for lo)
-              __half hv[8], lv[8];
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const int col = colg + j;
-                const int acc = (int)am[g + j] - (p.row_zp ? zp * p.col_cs[col] : 0);
-                const float v = acc == 0 ? 0.f : s_row * p.col_s[col] * (float)acc;
-                if (!(fabsf(v) <= 65504.f) && p.err) atomicOr(p.err, 8 /*ERR_LR_RANGE*/);
-                hv[j] = __float2half_rn(v);
-                lv[j] = __float2half_rn(v - __half2float(hv[j]));
-              }
-              *reinterpret_cast<uint4*>(o + colg) = *reinterpret_cast<const uint4*>(hv);
-              if (p.lo_off) *reinterpret_cast<uint4*>(o + p.lo_off + colg) = *reinterpret_cast<const uint4*>(lv);
-            } else {
-#pragma unroll
-              for (int j = 0; j < 8; ++j)
-                if (colg + j < p.N) g2_epi_lr1(p, orow, colg + j, (int)am[g + j], zp, s_row);
             }
           }
         } else {
