@@ -673,6 +673,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
           }
           continue;
         }
+        float y[32];
+        if (p.mode == G2_SPLIT) {  // g2_epi_split, column constants broadcast from one load per lane
+          const int cl = min(n0 + c0 + lane, p.N - 1);
+          const float sw_l = p.col_s[cl];
+          const int cs_l = p.row_zp ? p.col_cs[cl] : 0;
+          const float kap_l = has_aux ? p.col_kappa[cl] : 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float sw = __shfl_sync(0xffffffffu, sw_l, j);
+            const int cs = __shfl_sync(0xffffffffu, cs_l, j);
+            const float kap = __shfl_sync(0xffffffffu, kap_l, j);
+            float v = s_row * sw * (float)((int)am[j] - zp * cs);
+            if (has_aux) v = fmaf(rho * kap, __uint_as_float(af[j]), v);
+            y[j] = v;
+          }
+        }
         if (!row_ok) continue;
         if (p.mode == G2_ACC) {
           const int64_t so = (int64_t)(item % ksplit) * p.acc_slice;
@@ -697,12 +713,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
             }
           }
         } else {
-          float y[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = min(n0 + c0 + j, p.N - 1);
-            y[j] = g2_epi_split(p, col, (int)am[j], zp, s_row, rho, has_aux, __uint_as_float(af[j]));
-          }
           const int64_t base = (int64_t)row * p.ldo + n0 + c0;
           const bool full_chunk = (n0 + c0 + 32 <= p.N) && ((p.ldo & 7) == 0);
           if (p.out_dtype == G2_F32) {
