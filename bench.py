@@ -388,7 +388,7 @@ def run_ours(args):
         "per_projection": per_layer,
         "roofline": {
             "bound": "tensor",
-            "kernel": "splitq_gemm_kernel (split GEMM)",
+            "kernel": "splitq_gemm2_kernel (split GEMM)",
             "achieved": achieved_tops,
             "peak": peak_tops,
             "unit": "TFLOP/s",

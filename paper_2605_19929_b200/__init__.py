@@ -27,6 +27,7 @@ from .layer_io import (
 )
 from .lowrank import LowRankBranch, SvdFactors, build_branch, default_rank, truncated_svd
 from .mocd import ChannelPartition, MocdConfig, jaccard, outlier_set, select_topk, trivial_partition
+from .mocd_gpu import build_partition, channel_absmax, percentile_rank, text_score, vision_score
 from .calibrate import stability_report
 from .quantizer import (
     Granularity,
@@ -44,6 +45,8 @@ __all__ = [
     "AUX_BITS_FLOOR", "DEFAULT_ACT_SPEC", "DEFAULT_WEIGHT_SPEC", "SplitLayer", "build_layer",
     "forward", "forward_reference", "LowRankBranch", "SvdFactors", "build_branch",
     "default_rank", "truncated_svd", "ChannelPartition", "MocdConfig", "select_topk",
+    "build_partition", "vision_score", "percentile_rank", "text_score", "channel_absmax", "jaccard",
+    "stability_report", "TensorFormatError", "load_tensor", "save_tensor", "load_layer", "save_layer",
     "trivial_partition", "Granularity", "QuantParams", "QuantSpec", "compute_params",
     "fake_quantize", "quantize", "quantize_per_token", "ActivationBatch", "ModalityTag",
     "Transform", "diagonal_transform", "identity_transform", "init_transform",

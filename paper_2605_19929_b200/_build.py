@@ -41,19 +41,29 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit to an object in parallel (nvcc -c, one
+    process each), then link the shared library."""
     if not force and up_to_date():
         return LIB_PATH
-    cmd = [
-        _nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
-        "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=default",
-        "-o", LIB_PATH + ".tmp",
-        *[os.path.join(CSRC, s) for s in SOURCES],
-        "-lcudart",
-    ] + os.environ.get("SPLITQ_NVCC_EXTRA", "").split()
+    common = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+              "-Xcompiler", "-fvisibility=default"] + os.environ.get("SPLITQ_NVCC_EXTRA", "").split()
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True, cwd=CSRC)
+        common.insert(1, "-Xptxas=-v")
+    objdir = os.path.join(PKG_DIR, "build")
+    os.makedirs(objdir, exist_ok=True)
+    objs, procs = [], []
+    for src in SOURCES:
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+        objs.append(obj)
+        cmd = common + ["-c", "-o", obj, os.path.join(CSRC, src)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((cmd, subprocess.Popen(cmd, cwd=CSRC)))
+    for cmd, pr in procs:
+        if pr.wait() != 0:
+            raise subprocess.CalledProcessError(pr.returncode, cmd)
+    link = [_nvcc(), *ARCH, "-shared", "-o", LIB_PATH + ".tmp", *objs, "-lcudart"]
+    subprocess.run(link, check=True, cwd=CSRC)
     os.replace(LIB_PATH + ".tmp", LIB_PATH)
     return LIB_PATH
 

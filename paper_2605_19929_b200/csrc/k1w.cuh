@@ -112,7 +112,7 @@ __device__ __forceinline__ uint4 kw_ldg(const uint4* p) {
 }
 
 // exact reference code of m at scale S: clip(rha(fl64(m / S)) + zp, qmin, qmax)
-__device__ __noinline__ int kw_exact_code(double m, double S, int zp, int qmin, int qmax) {
+static __device__ __noinline__ int kw_exact_code(double m, double S, int zp, int qmin, int qmax) {
   const double v = __ddiv_rn(m, S);
   const double a = floor(__dadd_rn(fabs(v), 0.5));
   double q = (v < 0.0 ? -a : a) + (double)zp;

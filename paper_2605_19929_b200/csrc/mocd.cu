@@ -30,6 +30,8 @@
 namespace {
 
 }  // namespace
+#include "nvtx.cuh"
+
 extern "C" int splitq_internal_fail(int code, const char* msg);  // splitq_capi.cu
 namespace {
 
@@ -192,12 +194,14 @@ int launch_rc(const void* x, int64_t ld, const int* rows, const int* n_text, int
               const int* cand, int n_cand, uint16_t* counts, cudaStream_t s) {
   const size_t smem = rc_smem_bytes<T, ITEMS>();
   if (smem > 220 * 1024) return mfail(SPLITQ_ERR_UNSUPPORTED, "too many candidate channels");
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[64] = {};  // per device (the attribute is per context)
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return mfail(SPLITQ_ERR_CUDA, "cudaGetDevice");
+  if (dev < 0 || dev >= 64 || !attr[dev]) {
     if (cudaFuncSetAttribute(mocd_rank_counts_kernel<T, ITEMS>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return mfail(SPLITQ_ERR_CUDA, "cudaFuncSetAttribute (rank counts)");
-    attr = true;
+    if (dev >= 0 && dev < 64) attr[dev] = true;
   }
   mocd_rank_counts_kernel<T, ITEMS><<<(unsigned)max_text, RC_THREADS, smem, s>>>(
       x, ld, rows, n_text, cand, n_cand, counts);
@@ -666,6 +670,7 @@ extern "C" {
 int splitq_mocd_absmax(const void* x, int x_dtype, int64_t x_ld, const uint8_t* tags,
                        int64_t tokens, int64_t dim, double* vision_max, double* all_max,
                        int32_t* status, void* stream_) {
+  splitq::NvtxRange nv("splitq.mocd_absmax");
   if (!x || !tags || !vision_max || !all_max || !status)
     return mfail(SPLITQ_ERR_INVALID, "null argument");
   if (tokens <= 0 || dim <= 0) return mfail(SPLITQ_ERR_INVALID, "empty batch");
@@ -716,6 +721,7 @@ int splitq_mocd_absmax(const void* x, int x_dtype, int64_t x_ld, const uint8_t* 
 int splitq_mocd_rank_counts(const void* x, int x_dtype, int64_t x_ld, const int32_t* text_rows,
                             const int32_t* n_text, int64_t max_text, const int32_t* cand,
                             int64_t n_cand, uint16_t* counts, void* stream_) {
+  splitq::NvtxRange nv("splitq.mocd_rank_counts");
   if (!x || !text_rows || !n_text || !cand || !counts) return mfail(SPLITQ_ERR_INVALID, "null argument");
   if (n_cand <= 0) return mfail(SPLITQ_ERR_INVALID, "candidate channel set is empty");
   if (n_cand > 65535) return mfail(SPLITQ_ERR_UNSUPPORTED, "at most 65535 candidate channels");
@@ -744,6 +750,7 @@ int splitq_mocd_transpose_u16(const uint16_t* in, int64_t rows, int64_t cols, ui
 int splitq_mocd_text_score(const uint16_t* counts_t, int64_t ld, int64_t n_cand, int64_t n_text,
                            int k, int max_iter, int64_t c0, int64_t c1, double* scores,
                            void* stream_) {
+  splitq::NvtxRange nv("splitq.mocd_text_score");
   if (!counts_t || !scores) return mfail(SPLITQ_ERR_INVALID, "null argument");
   if (k < 1) return mfail(SPLITQ_ERR_INVALID, "cluster count must be positive");
   if (k > n_text) return mfail(SPLITQ_ERR_INVALID, "cluster count exceeds number of text tokens");
@@ -752,12 +759,14 @@ int splitq_mocd_text_score(const uint16_t* counts_t, int64_t ld, int64_t n_cand,
   const size_t bits = (size_t)(((n_cand + 32) / 32 * 4 + 15) & ~15);
   const size_t after = (size_t)TS_THREADS * 8 + (size_t)TS_THREADS * TS_KMAX * 4 + (size_t)(n_cand + 1);
   const size_t smem = bits + std::max((size_t)(n_cand + 1) * 4, after) + 16;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[64] = {};  // per device (the attribute is per context)
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return mfail(SPLITQ_ERR_CUDA, "cudaGetDevice");
+  if (dev < 0 || dev >= 64 || !attr[dev]) {
     if (cudaFuncSetAttribute(mocd_text_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              200 * 1024) != cudaSuccess)
       return mfail(SPLITQ_ERR_CUDA, "cudaFuncSetAttribute (text score)");
-    attr = true;
+    if (dev >= 0 && dev < 64) attr[dev] = true;
   }
   if (smem > 200 * 1024) return mfail(SPLITQ_ERR_UNSUPPORTED, "too many candidate channels");
   mocd_text_score_kernel<<<(unsigned)(c1 - c0), TS_THREADS, smem,
@@ -768,6 +777,7 @@ int splitq_mocd_text_score(const uint16_t* counts_t, int64_t ld, int64_t n_cand,
 
 int splitq_mocd_topk(const double* scores, int64_t n, int64_t k, int32_t* flags, int64_t* out,
                      void* stream_) {
+  splitq::NvtxRange nv("splitq.mocd_topk");
   if (!scores || !flags || !out) return mfail(SPLITQ_ERR_INVALID, "null argument");
   if (k > n) return mfail(SPLITQ_ERR_INVALID, "k exceeds score vector length");
   if (k <= 0 || n <= 0) return SPLITQ_OK;

@@ -95,7 +95,7 @@ __device__ __forceinline__ int8_t store_code(int q, int zp, const QSpecDev& s) {
 // ---------------------------------------------------------------- compaction
 // text_idx[i] = position of row i among text rows (or -1), text_rows[c] = i.
 // One CTA of 1024 threads, each owning a contiguous run of rows.
-__global__ void compact_text_rows_kernel(const uint8_t* __restrict__ tags, int T,
+static __global__ void compact_text_rows_kernel(const uint8_t* __restrict__ tags, int T,
                                          int* __restrict__ text_idx, int* __restrict__ text_rows,
                                          int* __restrict__ n_text, int* __restrict__ err) {
   __shared__ int warp_sums[32];
@@ -238,7 +238,7 @@ __device__ __forceinline__ void block_minmax(double& lo, double& hi, double* red
 }
 
 // Quantize one outlier path (n <= a few hundred columns) with one warp.
-__device__ void outlier_row(const K1Params& p, int row, const int* cols, const double* d, int n,
+static __device__ void outlier_row(const K1Params& p, int row, const int* cols, const double* d, int n,
                             int ld, int8_t* codes, double* s_out, float* sf_out, int* zp_out) {
   const int lane = threadIdx.x & 31;
   double lo = INFINITY, hi = -INFINITY;
@@ -282,7 +282,7 @@ __device__ void outlier_row(const K1Params& p, int row, const int* cols, const d
   }
 }
 
-__global__ void __launch_bounds__(K1_THREADS) k1_quantize_kernel(const K1Params p) {
+static __global__ void __launch_bounds__(K1_THREADS) k1_quantize_kernel(const K1Params p) {
   __shared__ double red[16];
   __shared__ double sh_S, sh_zp;
   const int row = blockIdx.x;

@@ -19,6 +19,7 @@
 #include <cuda_fp16.h>
 
 #include "quantize.cuh"
+#include "sm100_ptx.cuh"
 
 namespace splitq {
 
@@ -37,164 +38,13 @@ __device__ __forceinline__ double to_f64<float>(float v) { return (double)v; }
 template <>
 __device__ __forceinline__ double to_f64<double>(double v) { return v; }
 
-template <typename T>
-__device__ __forceinline__ bool finite_in(T v) {
-  return isfinite(to_f64(v));
-}
-
-// q = clip(rha(m / S) + zp, qmin, qmax) with the reference's rounding
-// (quantizer.py:76-77, 152-154); rS = 1 / S.
-__device__ __forceinline__ int quant_fast(double m, double S, double rS, int zp, int qmin,
-                                          int qmax) {
-  const double v = __dmul_rn(m, rS);
-  const double a = fabs(v);
-  int n;
-  if (__double2hiint(a) >= 0x41D00000) {  // |v| >= 2^30: saturates after clipping
-    n = 1 << 30;
-  } else {
-    const double t = __dadd_rn(a, K1_MAGIC);
-    const double diff = __dsub_rn(a, __dsub_rn(t, K1_MAGIC));  // a - RNE(a), in [-0.5, 0.5]
-    n = __double2loint(t);
-    if (diff > 0.499999 || diff < -0.499999) {  // near a tie: exact reference expression
-      const double ve = __ddiv_rn(m, S);
-      n = (int)floor(__dadd_rn(fabs(ve), 0.5));
-      return min(max((ve < 0.0 ? -n : n) + zp, qmin), qmax);
-    }
-  }
-  const int q = (__double2hiint(v) < 0 ? -n : n) + zp;
-  return min(max(q, qmin), qmax);
-}
-
-struct K1Smem {
-  // per-warp partial min / max of the current reduction
-  double red_lo[32], red_hi[32];
-  double red2_lo[32], red2_hi[32];
-  double xh[256];  // x_hat of every code level of the current row
-  int bad[2];      // per row parity: a non-finite x was seen
-};
-
-template <int EPT>
-struct K1Bounds {
-  static constexpr int max_threads = 512;         // host keeps NT <= 512
-  static constexpr bool cache_tables = EPT <= 8;  // gather table held in registers
-};
-
-__device__ __forceinline__ void reduce_minmax(double& lo, double& hi, double* slo, double* shi) {
-  const int NW = blockDim.x >> 5;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) {
-    slo[warp] = lo;
-    shi[warp] = hi;
-  }
-  __syncthreads();
-  lo = slo[0];
-  hi = shi[0];
-  for (int w = 1; w < NW; ++w) {
-    lo = fmin(lo, slo[w]);
-    hi = fmax(hi, shi[w]);
-  }
-}
-
-// Copy one x row (n elements of T) into SMEM with 16-B cp.async when aligned.
-template <typename T>
-__device__ __forceinline__ void stage_row_async(T* dst, const T* src, int n, bool aligned16) {
-  if (aligned16) {
-    const int nvec = (n * (int)sizeof(T)) / 16;
-    const char* s = reinterpret_cast<const char*>(src);
-    char* d = reinterpret_cast<char*>(dst);
-    for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(d + 16 * i)),
-                   "l"(s + 16 * i)
-                   : "memory");
-    }
-    for (int i = nvec * 16 / (int)sizeof(T) + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
-  } else {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-}
-
-// Outlier path of one row by one warp, reading x from SMEM.
-template <typename T>
-__device__ void outlier_row_smem(const K1Params& p, int row, const T* xs, const int* cols,
-                                 const double* d, int n, int ld, int8_t* codes, double* s_out,
-                                 float* sf_out, int* zp_out) {
-  const int lane = threadIdx.x & 31;
-  double lo = INFINITY, hi = -INFINITY;
-  for (int k = lane; k < n; k += 32) {
-    const double z = __dmul_rn(to_f64(xs[cols[k]]), d[k]);
-    lo = fmin(lo, z);
-    hi = fmax(hi, z);
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-  }
-  if (!isfinite(lo) || !isfinite(hi)) {
-    if (lane == 0) atomicOr(p.err, ERR_NONFINITE);
-    return;
-  }
-  double S, zpd;
-  if (!group_params(lo, hi, p.aux, &S, &zpd)) {
-    if (lane == 0) atomicOr(p.err, ERR_SCALE_ZERO);
-    S = 1.0;
-  }
-  const double rS = __ddiv_rn(1.0, S);
-  const int zp = (int)zpd;
-  int8_t* out = codes + (int64_t)row * ld;
-  for (int k = lane; k < ld; k += 32) {
-    int8_t c = 0;
-    if (k < n) {
-      const double z = __dmul_rn(to_f64(xs[cols[k]]), d[k]);
-      const int q = quant_fast(z, S, rS, zp, p.aux.qmin, p.aux.qmax);
-      c = p.aux.centered ? (int8_t)(q - zp) : (int8_t)(uint8_t)q;
-    }
-    out[k] = c;
-  }
-  if (lane == 0) {
-    s_out[row] = S;
-    sf_out[row] = (float)S;
-    zp_out[row] = zp;
-  }
-}
-
-// Exact-path fallback for quant_fast, kept out of line so the unrolled
-// element loops stay small.
-__device__ __noinline__ int quant_exact(double m, double S, double zp_qmin_qmax_packed_unused,
+// Exact reference expression clip(rha(m / S) + zp) (quantizer.py:76-77,
+// 152-154), kept out of line so the unrolled element loops stay small.
+static __device__ __noinline__ int quant_exact(double m, double S, double zp_qmin_qmax_packed_unused,
                                         int zp, int qmin, int qmax) {
   const double ve = __ddiv_rn(m, S);
   const int n = (int)floor(__dadd_rn(fabs(ve), 0.5));
   return min(max((ve < 0.0 ? -n : n) + zp, qmin), qmax);
-}
-
-// quant_fast without the inline slow path; see quant_fast for the contract.
-__device__ __forceinline__ int quant_lean(double m, double S, double rS, int zp, int qmin,
-                                          int qmax) {
-  const double v = __dmul_rn(m, rS);
-  const double a = fabs(v);
-  const double t = __dadd_rn(a, K1_MAGIC);
-  const double diff = __dsub_rn(a, __dsub_rn(t, K1_MAGIC));  // a - RNE(a)
-  int n = __double2loint(t);
-  // |v| >= 2^30 saturates after clipping; |diff| near 0.5 is a potential tie
-  if (__double2hiint(a) >= 0x41D00000) n = 1 << 30;
-  else if (fabs(diff) > 0.499999) return quant_exact(m, S, 0.0, zp, qmin, qmax);
-  const int q = (__double2hiint(v) < 0 ? -n : n) + zp;
-  return min(max(q, qmin), qmax);
-}
-
-__device__ __forceinline__ void minmax_upd(double z, double& lo, double& hi) {
-  lo = z < lo ? z : lo;  // NaN never enters (checked separately)
-  hi = z > hi ? z : hi;
 }
 
 __device__ __forceinline__ void warp_minmax(double& lo, double& hi) {
@@ -204,81 +54,6 @@ __device__ __forceinline__ void warp_minmax(double& lo, double& hi) {
     const double h2 = __shfl_xor_sync(0xffffffffu, hi, o);
     lo = l2 < lo ? l2 : lo;
     hi = h2 > hi ? h2 : hi;
-  }
-}
-
-// Gather 4 main elements k0..k0+3 of one row: z = x[c_main[k]] * d_main[k].
-// `full` = all four inside n_main (vector table loads); lanes outside get z = 0.
-template <typename T, bool GATHER>
-__device__ __forceinline__ void gather4(const K1Params& p, const T* xrow, int k0, bool full,
-                                        double (&z)[4]) {
-  if (full) {
-    int c[4];
-    double d[4];
-    if (GATHER) {
-      const int4 c4 = __ldg(reinterpret_cast<const int4*>(p.c_main + k0));
-      c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
-      const double2 d0 = __ldg(reinterpret_cast<const double2*>(p.d_main + k0));
-      const double2 d1 = __ldg(reinterpret_cast<const double2*>(p.d_main + k0 + 2));
-      d[0] = d0.x; d[1] = d0.y; d[2] = d1.x; d[3] = d1.y;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const double xv = to_f64(__ldg(xrow + (GATHER ? c[u] : k0 + u)));
-      z[u] = GATHER ? __dmul_rn(xv, d[u]) : xv;
-    }
-  } else {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int k = k0 + u;
-      z[u] = 0.0;
-      if (k < p.n_main) {
-        const double xv = to_f64(__ldg(xrow + (GATHER ? __ldg(p.c_main + k) : k)));
-        z[u] = GATHER ? __dmul_rn(xv, __ldg(p.d_main + k)) : xv;
-      }
-    }
-  }
-}
-
-// Outlier path of one row by one warp (x read through L1).
-template <typename T>
-__device__ void outlier_row_warp(const K1Params& p, int row, const T* xrow, const int* cols,
-                                 const double* d, int n, int ld, int8_t* codes, double* s_out,
-                                 float* sf_out, int* zp_out) {
-  const int lane = threadIdx.x & 31;
-  double lo = INFINITY, hi = -INFINITY;
-  bool nan = false;
-  for (int k = lane; k < n; k += 32) {
-    const double z = __dmul_rn(to_f64(__ldg(xrow + cols[k])), d[k]);
-    nan |= z != z;
-    lo = z < lo ? z : lo;
-    hi = z > hi ? z : hi;
-  }
-  warp_minmax(lo, hi);
-  if (__any_sync(0xffffffffu, nan) || !isfinite(lo) || !isfinite(hi)) {
-    if (lane == 0) atomicOr(p.err, ERR_NONFINITE);
-    return;
-  }
-  double S, zpd;
-  const bool ok = group_params(lo, hi, p.aux, &S, &zpd);
-  if (!ok) S = 1.0;
-  const double rS = __ddiv_rn(1.0, S);
-  const int zp = (int)zpd;
-  int8_t* out = codes + (int64_t)row * ld;
-  for (int k = lane; k < ld; k += 32) {
-    int c = 0;
-    if (k < n) {
-      const double z = __dmul_rn(to_f64(__ldg(xrow + cols[k])), d[k]);
-      const int q = quant_lean(z, S, rS, zp, p.aux.qmin, p.aux.qmax);
-      c = p.aux.centered ? q - zp : q;
-    }
-    out[k] = (int8_t)c;
-  }
-  if (lane == 0) {
-    if (!ok) atomicOr(p.err, ERR_SCALE_ZERO);
-    s_out[row] = S;
-    sf_out[row] = (float)S;
-    zp_out[row] = zp;
   }
 }
 
@@ -358,79 +133,6 @@ __device__ __forceinline__ void group_minmax(double& lo, double& hi, double* red
   }
 }
 
-template <typename T, bool GATHER>
-__device__ __forceinline__ void gather4_smem(const K1Params& p, const T* xs, int k0, bool full,
-                                             double (&z)[4]) {
-  if (full) {
-    int c[4];
-    double d[4];
-    if (GATHER) {
-      const int4 c4 = __ldg(reinterpret_cast<const int4*>(p.c_main + k0));
-      c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
-      const double2 d0 = __ldg(reinterpret_cast<const double2*>(p.d_main + k0));
-      const double2 d1 = __ldg(reinterpret_cast<const double2*>(p.d_main + k0 + 2));
-      d[0] = d0.x; d[1] = d0.y; d[2] = d1.x; d[3] = d1.y;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const double xv = to_f64(xs[GATHER ? c[u] : k0 + u]);
-      z[u] = GATHER ? __dmul_rn(xv, d[u]) : xv;
-    }
-  } else {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int k = k0 + u;
-      z[u] = 0.0;
-      if (k < p.n_main) {
-        const double xv = to_f64(xs[GATHER ? __ldg(p.c_main + k) : k]);
-        z[u] = GATHER ? __dmul_rn(xv, __ldg(p.d_main + k)) : xv;
-      }
-    }
-  }
-}
-
-// Outlier path of one row by one warp, x from the staged SMEM row.
-template <typename T>
-__device__ void outlier_row_sm(const K1Params& p, int row, const T* xs, const int* cols,
-                               const double* d, int n, int ld, int8_t* codes, double* s_out,
-                               float* sf_out, int* zp_out) {
-  const int lane = threadIdx.x & 31;
-  double lo = INFINITY, hi = -INFINITY;
-  bool nan = false;
-  for (int k = lane; k < n; k += 32) {
-    const double z = __dmul_rn(to_f64(xs[cols[k]]), d[k]);
-    nan |= z != z;
-    lo = z < lo ? z : lo;
-    hi = z > hi ? z : hi;
-  }
-  warp_minmax(lo, hi);
-  if (__any_sync(0xffffffffu, nan) || !isfinite(lo) || !isfinite(hi)) {
-    if (lane == 0) atomicOr(p.err, ERR_NONFINITE);
-    return;
-  }
-  bool ok;
-  const RowParams rp = make_row_params(lo, hi, p.aux, &ok);
-  int8_t* out = codes + (int64_t)row * ld;
-  for (int k = lane; k < ld; k += 32) {
-    int c = 0;
-    if (k < n) {
-      const double z = __dmul_rn(to_f64(xs[cols[k]]), d[k]);
-      bool tie = false;
-      int q = quant_row(z, rp, tie);
-      if (tie) q = quant_exact(z, rp.S, 0.0, rp.zp, rp.qmin, rp.qmax);
-      c = p.aux.centered ? q - rp.zp : q;
-    }
-    out[k] = (int8_t)c;
-  }
-  if (lane == 0) {
-    if (!ok) atomicOr(p.err, ERR_SCALE_ZERO);
-    s_out[row] = rp.S;
-    sf_out[row] = (float)rp.S;
-    zp_out[row] = rp.zp;
-  }
-}
-
-
 // ---- outlier paths in two steps: params (warp-level), then codes + the fp16
 // hi/lo segments of the auxiliary GEMM operand. a = (q - zp) * (S_p / rho) is
 // exact in fp64; a = a_hi + a_lo with a_hi = fp16(a), a_lo = fp16(a - a_hi).
@@ -479,7 +181,6 @@ __device__ void outlier_codes(const K1Params& p, int row, const T* xs, const int
     }
   }
 }
-
 
 // raw-bit finiteness test per input type: max of |bits| >= inf pattern
 template <typename T> struct InBits;
@@ -531,20 +232,6 @@ __device__ __forceinline__ void gather4_pad(const K1Params& p, const T* xs, int 
       z[u] = in ? to_f64(xv) : __longlong_as_double(0x7ff8000000000000ll);
     }
   }
-}
-
-// OR of a per-thread flag over the row group (red: >= 2 * G doubles of scratch)
-template <int G>
-__device__ __forceinline__ bool group_any_flag(bool v, double* red, int g, int wg) {
-  v = __any_sync(0xffffffffu, v);
-  if (G == 1) return v;
-  if ((threadIdx.x & 31) == 0) red[2 * wg] = v ? 1.0 : 0.0;
-  group_sync<G>(g);
-  double any = 0.0;
-#pragma unroll
-  for (int w = 0; w < G; ++w) any += red[2 * w];
-  group_sync<G>(g);
-  return any != 0.0;
 }
 
 // One row per group of G warps (K1G_WARPS / G rows per CTA). The row is

@@ -21,6 +21,7 @@
 #include "k1w.cuh"
 #include "gemv_decode.cuh"
 #include "tma_host.cuh"
+#include "nvtx.cuh"
 
 using namespace splitq;
 
@@ -210,10 +211,11 @@ int validate_index_set(const int64_t* c, int64_t n, int64_t dim, const char* nam
 }
 
 int check_codes(const int8_t* q, int64_t count, const QSpecDev& s, const char* name) {
-  // centred weight codes lie in [qmin - zp, qmax - zp] subset of [-(qmax-qmin), qmax-qmin]
-  const int lim = s.qmax - s.qmin;
+  // centred weight codes: symmetric in [qmin, qmax]; asymmetric in
+  // [qmin - zp, qmax - zp], a subset of [-(qmax-qmin), qmax-qmin]
+  const int lo = s.sym ? s.qmin : -(s.qmax - s.qmin), hi = s.sym ? s.qmax : s.qmax - s.qmin;
   for (int64_t i = 0; i < count; ++i)
-    if (q[i] < -lim || q[i] > lim) return fail(SPLITQ_ERR_INVALID, "%s code out of range", name);
+    if (q[i] < lo || q[i] > hi) return fail(SPLITQ_ERR_INVALID, "%s code out of range", name);
   return SPLITQ_OK;
 }
 
@@ -247,7 +249,11 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
   rc = make_spec(with_floor(d->act, floor_bits), &aux, "act_spec (aux floor)");
   if (!rc) rc = make_spec(with_floor(d->weight, floor_bits), &waux, "weight_spec (aux floor)");
   if (rc) return rc;
-  if (wsp.qmax - wsp.qmin > 127 || waux.qmax - waux.qmin > 127)
+  // centred weight codes must fit int8: symmetric codes lie in [qmin, qmax]
+  // (W8 sym: -127..127, the reference's DEFAULT_WEIGHT_SPEC, layer.py:41),
+  // asymmetric ones in [-(qmax - qmin), qmax - qmin]
+  auto w_fits = [](const QSpecDev& s) { return s.sym ? s.qmax <= 127 : s.qmax - s.qmin <= 127; };
+  if (!w_fits(wsp) || !w_fits(waux))
     return fail(SPLITQ_ERR_UNSUPPORTED, "weight codes must fit int8 (asymmetric 8-bit weights unsupported)");
   if (d->use_cws && (d->r_cws <= 0 || d->r_cws > std::min(d->n_main, d->d_out)))
     return fail(SPLITQ_ERR_INVALID, "branch rank exceeds min(path width, d_out)");
@@ -833,11 +839,13 @@ namespace {
 template <typename T, bool GA, int G>
 int launch_k1_g(const K1Params& k, int d_in, cudaStream_t stream) {
   const size_t smem = k1_group_smem(d_in, (int)sizeof(T), G);
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[64] = {};  // per device: the attribute is per-context
+  int device = 0;
+  CUDA_TRY(cudaGetDevice(&device));
+  if (device < 0 || device >= 64 || !attr[device]) {
     CUDA_TRY(cudaFuncSetAttribute(k1_group_kernel<T, GA, G>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    attr = true;
+    if (device >= 0 && device < 64) attr[device] = true;
   }
   constexpr int NG = K1G_WARPS / G;
   const unsigned grid = (unsigned)((k.T + NG - 1) / NG);
@@ -1094,7 +1102,10 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
     compact_text_rows_kernel<<<1, 1024, 0, stream>>>(tags, (int)T, text_idx, text_rows, n_text, err);
     CUDA_TRY(cudaGetLastError());
   }
-  if ((rc = launch_k1(k, (int)L->d_in, L->device, stream))) return rc;
+  {
+    NvtxRange r("splitq.K1");
+    if ((rc = launch_k1(k, (int)L->d_in, L->device, stream))) return rc;
+  }
   if (prof && (rc = prof_record(L, stream))) return rc;
 
   __half* lr_a = (__half*)at(W.lr_a);
@@ -1144,6 +1155,7 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
     if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (LR1)");
     return launch_gemm(g, L->device, T, stream, at(W.acc_scratch), W.acc_scratch_bytes);
   };
+  NvtxRange nv_lr1("splitq.LR1");
   if (gv && L->r_s && L->r_c) {  // decode: both first stages in one launch
     GvPlan ps, pc;
     if ((rc = lr1(at(W.a_main), L->act.centered, L->b_us, L->s_us, L->cs_us, L->r_s,
@@ -1169,6 +1181,7 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   if (prof && (rc = prof_record(L, stream))) return rc;
 
   // ---- split GEMM: int8 main GEMM + fp16 auxiliary GEMM + merge epilogue
+  nv_lr1.next("splitq.K2");
   GemmLaunch g{};
   const bool sw = use_swap(T);  // decode-sized: 256-row tiles over output channels
   g.p.M = (int)T;

@@ -168,6 +168,27 @@ def text_score_counts(counts, n_cand, k, max_iter=50):
     return _GPU.text_score(counts, n_cand, k, max_iter)
 
 
+def text_score(ranks, k, max_iter=50):
+    """text_score (mocd.py:141-150) with the reference's signature. The
+    device k-means runs on integer rank counts, so ``ranks`` must be
+    percentile_rank output: every entry an IEEE quotient count / n_cand with
+    n_cand = ranks.shape[1] (checked exactly; anything else raises)."""
+    torch = _torch()
+    on_dev = _is_torch(ranks)
+    r = ranks.detach().cpu().numpy() if on_dev else np.asarray(ranks, np.float64)
+    if r.ndim != 2:
+        raise ValueError(f"matrix must be 2-D, got ndim={r.ndim}")
+    n_cand = int(r.shape[1])
+    counts = np.rint(r * n_cand)
+    if n_cand == 0 or n_cand > 65535 or not np.array_equal(counts / n_cand, r) or np.any(counts < 1):
+        raise ValueError("text_score on the GPU takes percentile_rank output (counts / n_cand)")
+    from .runtime import device
+
+    c = torch.from_numpy(counts.astype(np.uint16).view(np.int16)).to(device())
+    out = text_score_counts(c, n_cand, k, max_iter)
+    return out if on_dev else out.cpu().numpy()
+
+
 def build_partition(batch, cfg: MocdConfig) -> ChannelPartition:
     """mocd.py:153-179 on the GPU (this process's batch, no collectives)."""
     return build_partition_distributed(batch.data, batch.tags, cfg, group=False)

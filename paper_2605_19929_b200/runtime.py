@@ -76,6 +76,10 @@ def pack_arrays(layer) -> dict:
     scales computed with the reference's own numpy expressions, so they are
     bit-exact by construction. Also the payload of a packed blob
     (layer_io.save_packed)."""
+    for name in ("p_main", "p_text", "p_vision"):
+        t = getattr(layer, name)
+        if not getattr(t, "is_diagonal", True) or getattr(t, "scale", None) is None:
+            raise ValueError("dense transforms are not supported on the GPU path")
     if _gran(layer.act_spec) != "per_token":
         raise ValueError("activation spec must be PER_TOKEN on the GPU path")
     if _gran(layer.weight_spec) == "per_token":
@@ -193,12 +197,22 @@ class GpuLayer:
         (f16/bf16/f32/f64, unit column stride), tags: CUDA uint8 [T]."""
         torch = _torch()
         lib = _lib.load()
+        if not (_is_torch(x) and _is_torch(tags)):
+            raise ValueError("run() takes CUDA tensors (use forward() for host arrays)")
+        if x.ndim != 2:
+            raise ValueError(f"matrix must be 2-D, got ndim={x.ndim}")
         T = int(x.shape[0])
         if x.shape[1] != self.d_in:
             raise ValueError("batch width does not match partition dim")
+        if x.device != self.device or tags.device != self.device:
+            raise ValueError(f"x and tags must be on {self.device}")
+        if x.dtype not in (torch.float16, torch.bfloat16, torch.float32, torch.float64):
+            raise ValueError(f"unsupported activation dtype {x.dtype}")
         if x.stride(1) != 1:
             x = x.contiguous()
-        tags = tags.to(torch.uint8)
+        tags = tags.reshape(-1).to(torch.uint8).contiguous()
+        if tags.numel() != T:
+            raise ValueError("tags length must match the number of rows")
         if ws is None:
             ws = self.workspace(T)
         if raw:
@@ -208,6 +222,11 @@ class GpuLayer:
             out_dtype = out_dtype or torch.float32
             if y is None:
                 y = torch.empty((T, self.d_out), dtype=out_dtype, device=self.device)
+            if (not _is_torch(y) or y.device != self.device or y.ndim != 2
+                    or tuple(y.shape) != (T, self.d_out) or y.stride(-1) != 1
+                    or y.dtype not in (torch.float32, torch.float16, torch.bfloat16)):
+                raise ValueError(f"y must be a CUDA f32/f16/bf16 [{T} x {self.d_out}] tensor with unit "
+                                 f"column stride on {self.device}")
             ydt = _dtype_code(y.dtype)
         y_ld = y.stride(-2)
         _lib.check(lib.splitq_forward(self.handle, _ptr(x), _dtype_code(x.dtype), x.stride(0),
@@ -233,20 +252,62 @@ class GpuLayer:
 _PACKED: dict = {}
 
 
+def _fingerprint(layer) -> bytes:
+    """Cheap content key of a layer: shapes, specs, the partition, the
+    smoothing scales, the branch gates and a strided sample of every weight
+    matrix. A layer whose arrays are edited in place after its first forward
+    (outside those samples) must be re-packed explicitly (GpuLayer(layer))."""
+    import hashlib
+
+    h = hashlib.blake2b(digest_size=16)
+    h.update(repr((layer.act_spec, layer.weight_spec, getattr(layer, "aux_bits_floor", None),
+                   bool(layer.use_cws), bool(layer.use_mac))).encode())
+
+    def put(a, sample=False):
+        if a is None:
+            h.update(b"-")
+            return
+        a = np.asarray(a)
+        h.update(repr((a.shape, a.dtype.str)).encode())
+        flat = a.reshape(-1)
+        if sample and flat.size > 65536:
+            flat = flat[:: flat.size // 65536 + 1]
+        h.update(np.ascontiguousarray(flat).tobytes())
+
+    p = layer.partition
+    for c in (p.c_main, p.c_text, p.c_vision):
+        put(c)
+    for t in (layer.p_main, layer.p_text, layer.p_vision):
+        put(getattr(t, "scale", None))
+    for w in (layer.w_main, layer.w_text, layer.w_vision):
+        put(w, sample=True)
+    for br in (getattr(layer, "branch_smooth", None), getattr(layer, "branch_comp", None)):
+        if br is not None:
+            put(br.gate)
+            put(br.u_star, sample=True)
+            put(br.v_base, sample=True)
+    return h.digest()
+
+
 def packed(layer) -> GpuLayer:
-    """Pack a layer once per (object, device); the cache entry dies with it."""
+    """Pack a layer once per (object, device, content fingerprint). Objects
+    without weakref support are not cached (their id may be reused)."""
     if isinstance(layer, GpuLayer):
         return layer
     dev = device()
+    try:
+        weakref.ref(layer)
+    except TypeError:
+        return GpuLayer(layer, dev)
     key = (id(layer), dev.index)
-    g = _PACKED.get(key)
-    if g is None:
-        g = GpuLayer(layer, dev)
-        _PACKED[key] = g
-        try:
-            weakref.finalize(layer, _PACKED.pop, key, None)
-        except TypeError:  # object without weakref support: keep it
-            pass
+    fp = _fingerprint(layer)
+    hit = _PACKED.get(key)
+    if hit is not None and hit[0] == fp:
+        return hit[1]
+    g = GpuLayer(layer, dev)
+    if hit is None:
+        weakref.finalize(layer, _PACKED.pop, key, None)
+    _PACKED[key] = (fp, g)
     return g
 
 

@@ -172,6 +172,11 @@ CASES = {
     "tiny_dout": dict(seed=17, T=64, d_in=128, d_out=12, k_t=4, k_v=4, r_s=2, r_c=3),
     # >= 64 n-tiles: m-fastest tile groups (G2Params.tile_gm)
     "wide_n": dict(seed=27, T=700, d_in=256, d_out=10400, k_t=8, k_v=8, r_s=8, r_c=8),
+    # the reference defaults: A8 asym PER_TOKEN x W8 sym PER_CHANNEL (layer.py:40-41)
+    "a8w8_default": dict(seed=28, T=300, d_in=640, d_out=256, k_t=32, k_v=32, r_s=10, r_c=15, abits=8,
+                         wbits=8),
+    "decode_t3_a8w8": dict(seed=29, T=3, d_in=512, d_out=256, k_t=16, k_v=16, r_s=8, r_c=8, abits=8,
+                           wbits=8, n_vision=1),
     # decode-sized calls (<= 8 rows): the CUDA-core GEMV kernels
     "decode_t2": dict(seed=18, T=2, d_in=512, d_out=384, k_t=16, k_v=16, r_s=16, r_c=16, n_vision=0),
     "decode_t5_a8": dict(seed=19, T=5, d_in=640, d_out=256, k_t=32, k_v=32, r_s=10, r_c=15, abits=8,
@@ -325,3 +330,32 @@ def test_gemv_multi_tile(name, monkeypatch):
     layer, x, tags = _case(**CASES[name])
     _check_acc(layer, x, tags)
     _check_out(layer, x, tags)
+
+
+def test_run_validates_buffers():
+    """GpuLayer.run rejects mismatched tags / outputs / devices before launching."""
+    from paper_2605_19929_b200 import runtime
+    layer, x, tags = _case(**CASES["tiny_dout"])
+    g = runtime.packed(layer)
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    td = torch.from_numpy(tags).cuda()
+    with pytest.raises(ValueError, match="tags length"):
+        g.run(xd, td[:-1])
+    with pytest.raises(ValueError, match="y must be"):
+        g.run(xd, td, y=torch.empty((x.shape[0] - 1, g.d_out), device="cuda"))
+    with pytest.raises(ValueError, match="y must be"):
+        g.run(xd, td, y=torch.empty((x.shape[0], g.d_out)))
+    with pytest.raises(ValueError, match="must be on"):
+        g.run(xd.cpu(), td)
+    y = g.run(xd, td)
+    assert y.shape == (x.shape[0], g.d_out)
+
+
+def test_packed_cache_sees_inplace_edits():
+    """An in-place edit of the layer's scales / gates re-packs it."""
+    from paper_2605_19929_b200 import runtime
+    layer, x, tags = _case(**CASES["tiny_dout"])
+    g1 = runtime.packed(layer)
+    assert runtime.packed(layer) is g1
+    layer.branch_smooth.gate[0] *= 0.5
+    assert runtime.packed(layer) is not g1
