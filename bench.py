@@ -7,14 +7,16 @@ Qwen2.5-VL-7B decoder projections (q, k, v, o, gate, up, down) at W4A4
 on, 32 + 32 outlier channels per layer input) over a batch of 8 samples x
 8192 tokens (1280 vision tokens in contiguous spans + 6912 text tokens per
 sample). One "step" = all seven projections over the whole batch. Under
-torchrun every rank runs its own batch of that size (token-sharded replicas,
-weak scaling: the units are independent token rows, so there is no
-collective on the path); `value` counts the tokens of all ranks.
+torchrun the batch's samples are sharded across the ranks (config 3:
+"tokens sharded across 1/2/4/8 GPUs"; strong scaling, no collective on the
+path since token rows are independent); ``--scaling weak`` gives every rank
+its own full batch instead. `value` counts the tokens of all ranks.
 
   value  tokens/s of the whole job (all ranks), device time, inputs resident in HBM
   e2e    same metric through the public API with host (pinned) inputs and outputs,
          H2D + D2H copies inside the timed region
-  roofline  split GEMM kernel vs the measured dense INT8 tensor peak
+  roofline  split GEMM kernel vs the measured dense INT8 tensor peak (burst)
+  roofline_k1  the stage-1 quantizer vs the measured HBM copy bandwidth
 
 ``--impl reference`` times the CPU oracle port (oracle/splitq_oracle.py, a
 restatement of the reference numpy path) on the same config; the reference
@@ -49,7 +51,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--tokens", type=int, default=SAMPLES * SEQ, help="tokens per rank per step")
+    ap.add_argument("--tokens", type=int, default=SAMPLES * SEQ,
+                    help="tokens per step: of the whole job (--scaling strong) or per rank (weak)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the batch's samples are sharded across the ranks (config 3); "
+                         "weak: every rank runs a full batch")
+    ap.add_argument("--no-fp32-out", action="store_true",
+                    help="skip the secondary fp32-output figure")
     ap.add_argument("--abits", type=int, default=4)
     ap.add_argument("--wbits", type=int, default=4)
     ap.add_argument("--no-e2e", action="store_true")
@@ -124,23 +132,28 @@ def measured_peaks():
 
 # ------------------------------------------------------------------ workload
 
-def build_workload(pkg, tokens, abits, wbits, seed=0, model="7b", vision_frac=None):
+def build_workload(pkg, tokens, abits, wbits, seed=0, model="7b", vision_frac=None, sample0=0):
     """Layer inputs (one per distinct projection input) and the 7 layers.
     Samples of SEQ tokens (or one sample of `tokens`), each with its vision
     tokens as contiguous image spans: 1280 of 8192 (config 3) by default,
-    3072 of 4096 for the 3B shapes (config 2)."""
-    rng = np.random.default_rng(seed)
+    3072 of 4096 for the 3B shapes (config 2). Each sample's tags come from
+    its global index (``sample0`` + i), so rank shards of a batch are the
+    batch's own samples; the layers come from their own stream and are the
+    same on every rank."""
     shape = wl.QWEN_3B if model == "3b" else wl.QWEN_7B
     if vision_frac is None:
         vision_frac = 0.75 if model == "3b" else VISION_PER_SAMPLE / SEQ
     specs = wl.model_specs(shape, abits=abits, wbits=wbits)
     seq = min(SEQ, tokens)
     n_samples = max(1, tokens // seq)
-    tags = np.concatenate([wl.tags_with_spans(rng, seq, int(round(vision_frac * seq)))
-                           for _ in range(n_samples)])[:tokens]
+    tags = np.concatenate([wl.tags_with_spans(np.random.default_rng((seed, 1, sample0 + i)), seq,
+                                              int(round(vision_frac * seq)))
+                           for i in range(n_samples)])[:tokens]
     if tags.shape[0] < tokens:  # non-multiple of SEQ
-        tags = np.concatenate([tags, wl.tags_with_spans(rng, tokens - tags.shape[0],
-                                                        (tokens - tags.shape[0]) * 5 // 32)])
+        rest = tokens - tags.shape[0]
+        tags = np.concatenate([tags, wl.tags_with_spans(np.random.default_rng((seed, 2, sample0)), rest,
+                                                        rest * 5 // 32)])
+    rng = np.random.default_rng(seed)
     inputs = {}
     groups = {"qkv": ("q", "k", "v"), "o": ("o",), "gu": ("gate", "up"), "down": ("down",)}
     layers = []
@@ -236,6 +249,8 @@ def run_ours(args):
 
     world, rank, local = dist_env()
     if world > 1:
+        # the communicator lines (ranks, NVLink / NVLS transport) for the driver's rank check
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -244,10 +259,18 @@ def run_ours(args):
     from paper_2605_19929_b200 import _lib, runtime
 
     lib = _lib.load()
-    tokens = args.tokens  # per rank (weak scaling: every rank runs one batch)
-    global_tokens = tokens * world
+    if args.scaling == "strong":  # the job's batch sharded by samples (rows are independent)
+        global_tokens = args.tokens
+        tokens = global_tokens // world
+        if tokens * world != global_tokens:
+            raise SystemExit(f"--tokens {global_tokens} does not split over {world} ranks")
+        sample0 = rank * max(1, tokens // SEQ)
+    else:  # every rank runs a full batch
+        tokens = args.tokens
+        global_tokens = tokens * world
+        sample0 = 0
     tags_all, inputs, layers = build_workload(pkg, tokens, args.abits, args.wbits, model=args.model,
-                                              vision_frac=args.vision_frac)
+                                              vision_frac=args.vision_frac, sample0=sample0)
     tags_np = np.ascontiguousarray(tags_all)
     tags = torch.from_numpy(tags_np).to(dev)
     xs = {g: make_input_tensor(torch, dev, tokens, inputs[g], tags_np, 1000 + 17 * rank + i)
@@ -334,12 +357,19 @@ def run_ours(args):
     # stage split and the roofline of the split GEMM (algorithmic int8 ops per launch)
     stage = np.zeros(3)
     gemm_ops = 0.0
+    k1_bytes = 0.0
     launches = 0
     per_layer = {}
+    n_text = int((tags_np == 0).sum())
     for g, sp, gl in packed:
         st_ms, calls = gl.profile_read()
         stage += np.array(st_ms)
         gemm_ops += 2.0 * tokens * sp.d_in * sp.d_out * calls
+        # K1 algorithmic bytes: fp16 rows in, main codes + the text
+        # rows' MAC codes + outlier codes + the aux operand row out
+        lay = gl.layout(tokens)
+        k1_bytes += calls * (tokens * sp.d_in * 2 + tokens * lay.ld_main + (n_text * lay.ld_main if sp.r_mac else 0)
+                             + tokens * (lay.ld_text + lay.ld_vision) + tokens * lay.k_lr * 2)
         launches += calls * (2 + (1 if sp.r_cws else 0) + (1 if sp.r_mac else 0))  # K1, LR1s, GEMM
         per_layer[sp.name] = {"quant_ms": st_ms[0] / max(calls, 1), "lr1_ms": st_ms[1] / max(calls, 1),
                               "gemm_ms": st_ms[2] / max(calls, 1),
@@ -348,11 +378,15 @@ def run_ours(args):
     achieved_tops = gemm_ops / (gemm_ms_total * 1e-3) / 1e12
     peaks = measured_peaks()
     int8 = peaks.get("int8") or {}
-    peak_tops = int8.get("int8_tops_sustained") or int8.get("int8_tops")
-    peak_src = "measured cuBLASLt int8 8192^3 (profiles/int8_peak.json, sustained)"
+    # burst (best single 8192^3 launch): the split GEMM launches are 0.1-5 ms
+    # each at full clocks, so the burst figure is the comparable peak
+    peak_tops = int8.get("int8_tops") or int8.get("int8_tops_sustained")
+    peak_src = "measured cuBLASLt int8 8192^3 burst (profiles/int8_peak.json)"
     if not peak_tops:
         peak_tops = DATASHEET_INT8_TOPS
         peak_src = "datasheet dense INT8 (no measured INT8 entry)"
+    hbm = float(peaks.get("hbm_gbs") or 6553.0)
+    k1_gbs = k1_bytes / (stage[0] * 1e-3) / 1e9 if stage[0] > 0 else None
 
     value = global_tokens * args.steps / (ms * 1e-3)
     result = {
@@ -364,7 +398,7 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "int8 (W4A4 codes on tcgen05 kind::i8, int32 accumulate)",
         "data": "synthetic (seeded N(0,1) fp16 activations with x30-x100 outlier channels; "
@@ -376,8 +410,10 @@ def run_ours(args):
                          "(A asym per-token, W sym per-channel), CWS+MAC on, K = 1% of D_in"),
             "global_tokens": global_tokens, "tokens_per_gpu": tokens,
             "samples": SAMPLES, "seq_len": SEQ, "vision_tokens_per_sample": VISION_PER_SAMPLE,
-            "parallelism": f"token-sharded replicas x{world}, one 8x8192-token batch per rank "
-                           "(no collective on the path)",
+            "parallelism": (f"dp{world}: the batch's samples sharded over {world} rank(s) "
+                            "(token rows are independent: no collective on the path)"
+                            if args.scaling == "strong" else
+                            f"dp{world} replicas, one 8x8192-token batch per rank (no collective on the path)"),
             "out_dtype": args.out_dtype, "abits": args.abits, "wbits": args.wbits,
             "schedule": (args.schedule + (": q||k||v, o, gate||up, down on parallel streams (own workspaces)"
                                           if args.schedule == "branches" else ": one stream")),
@@ -394,14 +430,52 @@ def run_ours(args):
             "unit": "TFLOP/s",
             "frac": achieved_tops / peak_tops,
             "peak_source": peak_src,
+            "frac_of_sustained": achieved_tops / (int8.get("int8_tops_sustained") or peak_tops),
             "frac_of_datasheet_4500": achieved_tops / DATASHEET_INT8_TOPS,
             "traffic": ncu_gemm_traffic(),
             "algorithmic_ops": "2*T*D_in*D_out per projection (dense-equivalent, SURVEY 8(d))",
+        },
+        "roofline_k1": {
+            "bound": "hbm",
+            "kernel": "k1w_kernel (stage-1 quantizer)",
+            "bytes_per_step": k1_bytes / args.steps,
+            "ms_per_step": stage[0] / args.steps,
+            "achieved": k1_gbs,
+            "peak": hbm,
+            "unit": "GB/s",
+            "frac": (k1_gbs / hbm) if k1_gbs else None,
+            "algorithmic_bytes": "T*D_in*2 in + T*ld (main codes) + T_text*ld (MAC codes) + outlier codes "
+                                 "+ T*k_lr*2 (aux operand) per projection",
         },
         "gpu_launches": launches,
         "clocks": clk,
     }
 
+    if not args.no_fp32_out and args.out_dtype != "float32":
+        # the same step with fp32 outputs (the parity bar's output type: F11 of
+        # SURVEY -- fp16 storage alone rounds by 2^-11 relative)
+        ys32 = [torch.empty((tokens, sp.d_out), dtype=torch.float32, device=dev) for _, sp, _ in packed]
+        ys_keep = list(ys)
+        ys[:] = ys32
+        step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.steps):
+            step()
+        s1.record(stream)
+        s1.synchronize()
+        ms32 = s0.elapsed_time(s1)
+        if world > 1:
+            t = torch.tensor([ms32], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms32 = float(t.item())
+        ys[:] = ys_keep
+        del ys32
+        result["value_fp32_out"] = {"value": global_tokens * args.steps / (ms32 * 1e-3), "unit": "tokens/s",
+                                    "ms_per_step": ms32 / args.steps}
     if not args.no_e2e:
         result["e2e"] = run_e2e(args, torch, dev, packed, xs, tags_np, ws, out_dt, global_tokens, world)
     if world > 1:

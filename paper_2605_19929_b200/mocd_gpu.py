@@ -92,20 +92,23 @@ class GpuStats:
                                                counts.data_ptr(), _stream()))
         return counts
 
-    def text_score(self, counts, n_cand, k, max_iter, c0=0, c1=None):
-        """fp64 [n_cand] (entries [c0, c1) filled): _kmeans_1d of every channel."""
+    def text_score(self, counts, n_cand, k, max_iter):
+        """fp64 [w]: _kmeans_1d of each of the w columns of ``counts``
+        [n_text x w] (a column range of the percentile_rank numerators over
+        n_cand candidates: n_cand is the ranks' denominator)."""
         torch = _torch()
         lib = _lib.load()
-        n_text = counts.shape[0]
-        c1 = n_cand if c1 is None else c1
+        n_text, w = int(counts.shape[0]), int(counts.shape[1])
         # rows padded to 8 tokens: the kernel reads them as 16-byte vectors
-        counts_t = torch.empty((n_cand, max((n_text + 7) // 8 * 8, 8)), dtype=torch.int16,
+        counts_t = torch.empty((w, max((n_text + 7) // 8 * 8, 8)), dtype=torch.int16,
                                device=counts.device)
-        _lib.check(lib.splitq_mocd_transpose_u16(counts.data_ptr(), n_text, n_cand,
+        if not counts.is_contiguous():
+            counts = counts.contiguous()
+        _lib.check(lib.splitq_mocd_transpose_u16(counts.data_ptr(), n_text, w,
                                                  counts_t.data_ptr(), counts_t.stride(0), _stream()))
-        scores = torch.zeros(n_cand, dtype=torch.float64, device=counts.device)
-        _lib.check(lib.splitq_mocd_text_score(counts_t.data_ptr(), counts_t.stride(0), n_cand,
-                                              n_text, int(k), int(max_iter), int(c0), int(c1),
+        scores = torch.zeros(w, dtype=torch.float64, device=counts.device)
+        _lib.check(lib.splitq_mocd_text_score(counts_t.data_ptr(), counts_t.stride(0), int(n_cand),
+                                              n_text, int(k), int(max_iter), 0, w,
                                               scores.data_ptr(), _stream()))
         return scores
 
@@ -240,14 +243,18 @@ def build_partition_distributed(x_local, tags_local, cfg: MocdConfig, group=None
         if not all_flag(np.any(tags_np == 0)):
             raise ValueError("nonzero text ratio but no text tokens")
         counts = stats.rank_counts(x_local, tags_local, remaining)
-        if distributed:
-            counts = _gather_rows(counts, world, group)
-        n_text = int(counts.shape[0])
         n_cand = remaining.size
+        if distributed:
+            # channel-sharded k-means: every rank receives, for its own channel
+            # range, the counts of all text rows in token (= rank) order
+            counts, c0, c1 = _exchange_columns(counts, n_cand, world, rank, group)
+        else:
+            c0, c1 = 0, n_cand
+        n_text = int(counts.shape[0])
         k = min(cfg.clusters_k, n_text)
-        c0 = rank * n_cand // world
-        c1 = (rank + 1) * n_cand // world
-        scores = stats.text_score(counts, n_cand, k, cfg.kmeans_max_iter, c0, c1)
+        part = stats.text_score(counts, n_cand, k, cfg.kmeans_max_iter)
+        scores = torch.zeros(n_cand, dtype=torch.float64, device=part.device)
+        scores[c0:c1] = part
         if distributed:  # each rank filled its channel range, the rest is zero
             dist.all_reduce(scores, op=dist.ReduceOp.SUM, group=group)
         c_text = remaining[np.asarray(_to_np(stats.topk(scores, k_t)), np.int64)]
@@ -264,6 +271,36 @@ def _to_np(t):
 def _coll_device(stats):
     torch = _torch()
     return torch.device("cuda", torch.cuda.current_device()) if stats is _GPU else torch.device("cpu")
+
+
+def _exchange_columns(local, n_cand, world, rank, group):
+    """All-to-all of the rank-count matrix: rank q gets columns
+    [q n / W, (q + 1) n / W) of every rank's rows, stacked in rank (= token)
+    order. Each rank receives n_text x n / W counts instead of the whole
+    n_text x n matrix an all-gather would land on it (7.4 GB per
+    rank at D = 18944)."""
+    torch = _torch()
+    import torch.distributed as dist
+
+    n = torch.tensor([local.shape[0]], dtype=torch.int64, device=local.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    rows = [int(v.item()) for v in sizes]
+    bounds = [q * n_cand // world for q in range(world + 1)]
+    c0, c1 = bounds[rank], bounds[rank + 1]
+    esz = local.element_size()
+    # NCCL / gloo have no 16-bit integer collectives: move the raw bytes
+    send = torch.cat([local[:, bounds[q]:bounds[q + 1]].contiguous().reshape(-1).view(torch.uint8)
+                      for q in range(world)])
+    in_splits = [local.shape[0] * (bounds[q + 1] - bounds[q]) * esz for q in range(world)]
+    out_splits = [r * (c1 - c0) * esz for r in rows]
+    recv = torch.empty(sum(out_splits), dtype=torch.uint8, device=local.device)
+    dist.all_to_all_single(recv, send, out_splits, in_splits, group=group)
+    blocks, off = [], 0
+    for r, b in zip(rows, out_splits):
+        blocks.append(recv[off:off + b].view(local.dtype).view(r, c1 - c0))
+        off += b
+    return torch.cat(blocks, dim=0), c0, c1
 
 
 def _gather_rows(local, world, group):

@@ -64,9 +64,12 @@ def test_sampled_rows_match_oracle(proj):
     ref = orc.forward(L, xs, ts)
     got = y[torch.from_numpy(rows).to(dev)].cpu().numpy()
     rms = np.sqrt(np.mean(ref ** 2))
-    # fp16 output storage: one rounding (2^-11 relative) on top of the bar
-    excess = np.abs(got - ref) - 2.0 ** -11 * np.abs(ref)
-    assert np.max(excess) <= 1e-3 * rms
+    # fp32 output (GpuLayer.run's default): the north-star bar, no slack
+    assert np.max(np.abs(got - ref)) <= 1e-3 * rms
+    # fp16 output storage: the same bar after one rounding of the output
+    # type (unit roundoff 2^-11); stated separately because |y| reaches ~6 rms
+    y16 = gl.run(x, td, out_dtype=torch.float16)[torch.from_numpy(rows).to(dev)].double().cpu().numpy()
+    assert np.max(np.abs(y16 - ref) - 2.0 ** -11 * np.abs(ref)) <= 1e-3 * rms
 
 
 def test_chunks_through_every_regime_bit_identical(proj):

@@ -109,14 +109,11 @@ class OracleStats:
         from oracle import mocd_oracle as mo
         return torch.from_numpy(mo.rank_counts(x, tags, cand).astype(np.int16))
 
-    def text_score(self, counts, n_cand, k, max_iter, c0=0, c1=None):
+    def text_score(self, counts, n_cand, k, max_iter):
         from oracle import mocd_oracle as mo
-        c1 = n_cand if c1 is None else c1
         cnt = counts.numpy().astype(np.int64) & 0xFFFF
-        out = np.zeros(n_cand)
-        for c in range(c0, c1):
-            out[c] = mo.kmeans_1d_exact(cnt[:, c], n_cand, k, max_iter)
-        return torch.from_numpy(out)
+        return torch.from_numpy(np.array([mo.kmeans_1d_exact(cnt[:, c], n_cand, k, max_iter)
+                                          for c in range(cnt.shape[1])]))
 
     def topk(self, scores, k):
         from oracle import mocd_oracle as mo
@@ -151,5 +148,32 @@ def test_mocd_partition_distributed_equals_single_process():
     x, tags = _mocd_case()
     ref = mo.build_partition(x, tags, 0.1, 0.1, 3)
     for out in spawn(_sharded_partition):
+        for a, b in zip(out, ref):
+            np.testing.assert_array_equal(a, b)
+
+
+def _exchange(rank, world):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2605_19929_b200 import mocd_gpu
+    full = torch.arange(23 * 10, dtype=torch.int16).view(23, 10)
+    bounds = [r * 23 // world for r in range(world + 1)]  # uneven row shards
+    got, c0, c1 = mocd_gpu._exchange_columns(full[bounds[rank]:bounds[rank + 1]].clone(), 10, world, rank, None)
+    return got.numpy(), c0, c1
+
+
+def test_rank_count_column_exchange_world3():
+    """The all-to-all gives each rank its channel range of every row, in
+    token order (uneven row and column splits)."""
+    full = np.arange(23 * 10, dtype=np.int16).reshape(23, 10)
+    for got, c0, c1 in spawn(_exchange, world=3):
+        np.testing.assert_array_equal(got, full[:, c0:c1])
+
+
+def test_mocd_partition_distributed_world3():
+    from oracle import mocd_oracle as mo
+    x, tags = _mocd_case()
+    ref = mo.build_partition(x, tags, 0.1, 0.1, 3)
+    for out in spawn(_sharded_partition, world=3):
         for a, b in zip(out, ref):
             np.testing.assert_array_equal(a, b)
