@@ -14,6 +14,8 @@ from .layer import (
     build_layer,
     forward,
     forward_reference,
+    forward_with_cache,
+    with_updated_params,
 )
 from .layer_io import (
     TensorFormatError,
@@ -29,6 +31,8 @@ from .lowrank import LowRankBranch, SvdFactors, build_branch, default_rank, trun
 from .mocd import ChannelPartition, MocdConfig, jaccard, outlier_set, select_topk, trivial_partition
 from .mocd_gpu import build_partition, channel_absmax, percentile_rank, text_score, vision_score
 from .calibrate import stability_report
+# after the submodule import: ``calibrate`` names the function, as in modquant
+from .calib_gpu import CalibConfig, LossTrace, NonFiniteLossError, calibrate
 from .quantizer import (
     Granularity,
     QuantParams,
@@ -46,7 +50,8 @@ __all__ = [
     "forward", "forward_reference", "LowRankBranch", "SvdFactors", "build_branch",
     "default_rank", "truncated_svd", "ChannelPartition", "MocdConfig", "select_topk",
     "build_partition", "vision_score", "percentile_rank", "text_score", "channel_absmax", "jaccard",
-    "stability_report", "TensorFormatError", "load_tensor", "save_tensor", "load_layer", "save_layer",
+    "stability_report", "TensorFormatError", "forward_with_cache", "with_updated_params", "CalibConfig",
+    "LossTrace", "NonFiniteLossError", "calibrate", "load_tensor", "save_tensor", "load_layer", "save_layer",
     "trivial_partition", "Granularity", "QuantParams", "QuantSpec", "compute_params",
     "fake_quantize", "quantize", "quantize_per_token", "ActivationBatch", "ModalityTag",
     "Transform", "diagonal_transform", "identity_transform", "init_transform",

@@ -10,7 +10,7 @@ accepted, so a ``modquant.layer.SplitLayer`` drops in unchanged.
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
 
 import numpy as np
 
@@ -151,3 +151,28 @@ def forward_reference(w, batch):
         raise ValueError(f"dimension mismatch: {tuple(xt.shape)} @ {tuple(wt.shape)}")
     y = xt @ wt
     return y if _is_torch(x) else y.cpu().numpy()
+
+
+def forward_with_cache(layer, batch):
+    """layer.py:118-172 on the device: (y fp64 CUDA tensor, cache of fp64 CUDA
+    tensors) -- the calibration caller's forward (calib_gpu.py)."""
+    from . import calib_gpu
+
+    return calib_gpu.forward_with_cache(layer, batch)
+
+
+def with_updated_params(layer, p_main=None, p_text=None, p_vision=None, gate_smooth=None,
+                        gate_comp=None):
+    """layer.py:355-375: a copy with selected learnable parameters replaced."""
+    changes = {}
+    if p_main is not None:
+        changes["p_main"] = p_main
+    if p_text is not None:
+        changes["p_text"] = p_text
+    if p_vision is not None:
+        changes["p_vision"] = p_vision
+    if gate_smooth is not None:
+        changes["branch_smooth"] = layer.branch_smooth.with_gate(gate_smooth)
+    if gate_comp is not None:
+        changes["branch_comp"] = layer.branch_comp.with_gate(gate_comp)
+    return replace(layer, **changes)

@@ -213,7 +213,44 @@ def gen_stability():
          mean=np.array([r["mean_jaccard"] for r in rep]), std=np.array([r["std_jaccard"] for r in rep]))
 
 
+def gen_calib():
+    """The reference's calibration caller (calibrate.py:146-270) on layers of
+    the gen_layers recipe: loss + analytic straight-through gradient at the
+    initial parameters, and a short calibrate() run (loss trace + final
+    parameters)."""
+    import importlib
+    cal = importlib.import_module("modquant.calibrate")
+    out = {}
+    idx = 0
+    for seed in range(2):
+        batch = generate(SynthConfig(tokens_text=24, tokens_vision=16, dim=48,
+                                     vision_outlier_channels=(1, 7),
+                                     text_outlier_channels=(5, 30), seed=seed))
+        w = generate_weight(48, 40, seed=seed + 10_000)
+        part = mocd.build_partition(batch, mocd.MocdConfig(ratio_vision=2 / 48, ratio_text=2 / 48))
+        for abits, wbits, cws, mac in ((4, 4, True, True), (3, 3, True, False), (4, 4, False, True)):
+            act = QuantSpec(abits, False, Granularity.PER_TOKEN)
+            wsp = QuantSpec(wbits, True, Granularity.PER_CHANNEL)
+            layer = L.build_layer(w, batch, part, act, wsp, use_cws=cws, use_mac=mac)
+            cfg = cal.CalibConfig(steps=6)
+            segments = cal._param_layout(layer, cfg)
+            y_ref = L.forward_reference(layer.full_weight(), batch)
+            loss, grad = cal.analytic_gradient(layer, batch, segments, y_ref)
+            final, trace = cal.calibrate(layer, batch, cfg)
+            pre = f"C{idx}_"
+            out.update(layer_arrays(layer, pre))
+            out[pre + "x"] = batch.data
+            out[pre + "tags"] = batch.tags
+            out[pre + "loss"] = np.array(loss)
+            out[pre + "grad"] = grad
+            out[pre + "trace"] = np.array(trace.losses)
+            out[pre + "theta"] = cal._initial_params(final, segments)
+            idx += 1
+    out["n_layers"] = np.array(idx)
+    save("calib.npz", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["quantizer", "layers", "config1", "mocd", "layer_dir", "stability"]
+    which = sys.argv[1:] or ["quantizer", "layers", "config1", "mocd", "layer_dir", "stability", "calib"]
     for name in which:
         globals()["gen_" + name]()

@@ -24,9 +24,9 @@ def _inputs(i):
     wm = G[p + "w_main"]
     w = np.empty((dim, wm.shape[1]))
     w[c_m], w[c_t], w[c_v] = wm, G[p + "w_text"], G[p + "w_vision"]
-    ab, asym, wb, wsym, cws, mac, _floor = (int(v) for v in G[p + "specs"])
-    act = pkg.QuantSpec(ab, bool(asym), pkg.Granularity.PER_TOKEN)
-    wsp = pkg.QuantSpec(wb, bool(wsym), pkg.Granularity.PER_CHANNEL)
+    ab, a_sym, wb, w_sym, cws, mac, _floor = (int(v) for v in G[p + "specs"])
+    act = pkg.QuantSpec(ab, bool(a_sym), pkg.Granularity.PER_TOKEN)
+    wsp = pkg.QuantSpec(wb, bool(w_sym), pkg.Granularity.PER_CHANNEL)
     part = pkg.ChannelPartition(c_m, c_t, c_v, dim)
     batch = pkg.ActivationBatch(G[p + "x"], G[p + "tags"])
     return pkg, w, batch, part, act, wsp, bool(cws), bool(mac)
