@@ -187,10 +187,12 @@ int splitq_mocd_rank_counts(const void* x, int x_dtype, int64_t x_ld, const int3
 /* out[c][r] = in[r][c] (uint16), out row stride ld_out. */
 int splitq_mocd_transpose_u16(const uint16_t* in, int64_t rows, int64_t cols, uint16_t* out,
                               int64_t ld_out, void* stream);
-/* text_score (mocd.py:141-150) for candidate channels [c0, c1): _kmeans_1d
- * (mocd.py:114-138) of counts_t[c][0..n_text) / n_cand, evaluated with
- * numpy's exact float64 arithmetic (quantile init, pairwise-sum means).
- * counts_t: uint16 [n_cand x ld] (transposed counts); scores fp64 [n_cand]. */
+/* text_score (mocd.py:141-150) for the channel rows [c0, c1) of counts_t:
+ * _kmeans_1d (mocd.py:114-138) of counts_t[c][0..n_text) / n_cand,
+ * evaluated with numpy's exact float64 arithmetic (quantile init,
+ * pairwise-sum means). counts_t: uint16 [>= c1 x ld] (transposed counts of
+ * a channel range); n_cand: the rank denominator |C'| (the counts lie in
+ * 1..n_cand); scores fp64, scores[c] written for c in [c0, c1). */
 int splitq_mocd_text_score(const uint16_t* counts_t, int64_t ld, int64_t n_cand, int64_t n_text,
                            int k, int max_iter, int64_t c0, int64_t c1, double* scores,
                            void* stream);

@@ -167,23 +167,6 @@ __device__ __forceinline__ void kw_ext_upd(KwExt& e, float cm, int j) {
   e.m1 = better ? cm : e.m1;
 }
 
-__device__ __forceinline__ double kw_warp_min_d(double v) {
-  const unsigned m = __ballot_sync(0xffffffffu, v < INFINITY);
-  if (m == 0) return INFINITY;
-  if ((m & (m - 1)) == 0) return kw_shfl_d(v, __ffs(m) - 1);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-__device__ __forceinline__ double kw_warp_max_d(double v) {
-  const unsigned m = __ballot_sync(0xffffffffu, v > -INFINITY);
-  if (m == 0) return -INFINITY;
-  if ((m & (m - 1)) == 0) return kw_shfl_d(v, __ffs(m) - 1);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
 template <typename T>
 __device__ __forceinline__ void kw_load(const K1Params& p, const uint4* xg, int j, float (&x)[8],
                                         float (&d)[8]) {

@@ -51,6 +51,10 @@ inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 // tile N: up to 160 with the fp32 aux accumulator (two main buffers + one aux
 // buffer = 3 bn TMEM columns), up to 256 without it (two main buffers)
 int tile_n(int64_t n, bool aux) {
+  if (const char* e = getenv("SPLITQ_TILE_N")) {  // experiments: force the tile width
+    const int f = atoi(e);
+    if (f >= 32 && f % 32 == 0 && f <= (aux ? G2_BN : G2_BN_MAX)) return f;
+  }
   if (aux) {  // 160-wide tiles unless the last tile would waste > 5 % of the columns
     const int64_t r160 = round_up(n, G2_BN);
     if (n > 128 && r160 * 100 > n * 105) return 128;
