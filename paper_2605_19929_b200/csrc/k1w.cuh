@@ -17,15 +17,17 @@
 //    tracks its best and second-best 8-element chunk extremes; only chunks
 //    within a 2^-21 band of the warp's fp32 extreme can hold the exact one,
 //    and those are recomputed in fp64.
-//  * codes: t = fl32(fl32(z32 fl32(1/S)) + C), C = 1.5*2^k + 0.5 + W ulp
-//    (+ zp for uncentred storage), puts floor(v + 0.5) in the integer bits
-//    of t. |t - (v_ref + C)| <= vmax 2^-21 + ulp / 2 < W ulp, so unless the
+//  * codes: t = fl32(z32 fl32(1/S) + C) (one fused rounding), C = 1.5*2^k +
+//    0.5 + W ulp (+ zp for uncentred storage), puts floor(v + 0.5) in the
+//    integer bits of t. |t - (v_ref + C)| <= vmax 2^-21 + ulp / 2 < W ulp
+//    (the bound holds for the two-rounding form too), so unless the
 //    fractional bits of t lie within 2W ulp of the tie point (then: exact
 //    fp64 recompute), floor(t) matches the reference's sign(v)floor(|v|+.5)
 //    (the fl64(|v| + 0.5) rounding only matters inside that window). The
 //    code byte is (bits(t) >> (23 - k)) & 0xFF since 2^(k-1) = 0 mod 256.
 //  * MAC residual (text rows): e = z - fl64(n S) is exact (Sterbenz) and
-//    e / S = v - n, so f = fl32(v32 - n) has v32's absolute error bound and
+//    e / S = v - n, so f = fl32(z32 fl32(1/S) - n) has v32's absolute error
+//    bound (plus one rounding of |f| <= 1/2) and
 //    e / S_e = f (S / S_e) is coded the same way; its exact extremes come
 //    from the same band-and-recompute step.
 #pragma once
@@ -235,28 +237,28 @@ __device__ __forceinline__ void kw_mulz(const float (&x)[8], const float (&d)[8]
   }
 }
 
-// v32 and the t bits of a chunk from its z32 (bit-identical in every pass)
-__device__ __forceinline__ void kw_vt(const float (&z)[8], const KwConsts& c, float (&v)[8],
-                                      uint32_t (&b)[8]) {
+// the t bits of a chunk from its z32: t = fl32(z32 rs + C), one rounding
+// (bit-identical in every pass). The window of kw_consts2 was derived for
+// fl32(fl32(z32 rs) + C); the fused form's error is no larger.
+__device__ __forceinline__ void kw_vt(const float (&z)[8], const KwConsts& c, uint32_t (&b)[8]) {
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
-    const float2 vv = kw_mul2(make_float2(z[2 * h], z[2 * h + 1]), make_float2(c.rs, c.rs));
-    const float2 t = kw_add2(vv, make_float2(c.C, c.C));
-    v[2 * h] = vv.x;
-    v[2 * h + 1] = vv.y;
+    const float2 t = kw_fma2(make_float2(z[2 * h], z[2 * h + 1]), make_float2(c.rs, c.rs), make_float2(c.C, c.C));
     b[2 * h] = __float_as_uint(t.x);
     b[2 * h + 1] = __float_as_uint(t.y);
   }
 }
 
-// f = v - n for the chunk (n from the integer bits of t)
-__device__ __forceinline__ void kw_frac(const float (&v)[8], const uint32_t (&b)[8], const KwConsts& c,
+// f = fl32(z32 rs - n) for the chunk (n from the integer bits of t; the
+// product is not rounded before the subtraction, so f carries only z32's
+// error, |f - (v - n)| <= |v| 2^-22.4 + 2^-25)
+__device__ __forceinline__ void kw_frac(const float (&z)[8], const uint32_t (&b)[8], const KwConsts& c,
                                         float (&f)[8]) {
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
     const float2 nf = kw_add2(make_float2(__uint_as_float(b[2 * h] & ~c.fm), __uint_as_float(b[2 * h + 1] & ~c.fm)),
                               make_float2(-c.base, -c.base));
-    const float2 ff = kw_add2(make_float2(v[2 * h], v[2 * h + 1]), make_float2(-nf.x, -nf.y));
+    const float2 ff = kw_fma2(make_float2(z[2 * h], z[2 * h + 1]), make_float2(c.rs, c.rs), make_float2(-nf.x, -nf.y));
     f[2 * h] = ff.x;
     f[2 * h + 1] = ff.y;
   }
@@ -785,17 +787,17 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
         KwRaw cur = pe;
         if (PF && j + GT < nchunks) pe = kw_ldraw(p, xg, j + GT);
         if (j < nchunks) {
-          float z[8], v[8], x[8], d[8];
+          float z[8], x[8], d[8];
           uint32_t b[8];
           if constexpr (PF) kw_cvt<T>(cur, x, d);
           else kwl(j, x, d);
           kw_mulz(x, d, z);
-          kw_vt(z, c, v, b);
+          kw_vt(z, c, b);
           *reinterpret_cast<uint2*>(arow + 8 * j) = kw_pack_shift(b, c.F);
           flag = kw_minfrac(b, c.fm) <= c.W2;
           if (mac) {
             float f[8], nf[8];
-            kw_frac(v, b, c, f);
+            kw_frac(z, b, c, f);
             if (SMF) {  // f * 2^15 rounded, offset-binary u16 (|f| < 1 off the flagged window)
               uint32_t u[8];
 #pragma unroll
@@ -874,12 +876,12 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
     if (!allx && (flo.m1 <= bfl || fhi.m1 <= bfh)) {
       const bool all = flo.m2 <= bfl || fhi.m2 <= bfh || (flo.m1 <= bfl && fhi.m1 <= bfh && flo.c1 != fhi.c1);
       for (int j = all ? gl : (flo.m1 <= bfl ? flo.c1 : fhi.c1); j < nchunks; j += GT) {
-        float f[8], x[8], d[8], z[8], v[8];
+        float f[8], x[8], d[8], z[8];
         uint32_t b[8];
         kwl(j, x, d);
         kw_mulz(x, d, z);
-        kw_vt(z, c, v, b);
-        kw_frac(v, b, c, f);
+        kw_vt(z, c, b);
+        kw_frac(z, b, c, f);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           if (f[u] <= bfl || -f[u] <= bfh) {
@@ -992,7 +994,6 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
         if (PG && j + GT < nchunks) pg = kw_ldraw(p, xg, j + GT);
         if (j < nchunks) {
           uint32_t be[8];
-          bool mflag = false;
           if (SMF && use_smf) {  // f from the 16-bit SMEM copy (pass-E-flagged chunks are queued)
             const uint4 w = fs[j];
             const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
@@ -1007,14 +1008,15 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
               be[2 * h + 1] = __float_as_uint(t.y);
             }
           } else {
-            float f[8], x[8], d[8], z[8], v[8];
+            // (chunks whose main codes were flagged in pass E are still in the
+            // queue: qn starts at qnE, so their MAC codes are exact-coded too)
+            float f[8], x[8], d[8], z[8];
             uint32_t b[8];
             if constexpr (PG) kw_cvt<T>(cur, x, d);
             else kwl(j, x, d);
             kw_mulz(x, d, z);
-            kw_vt(z, c, v, b);
-            kw_frac(v, b, c, f);
-            mflag = kw_minfrac(b, c.fm) <= c.W2;
+            kw_vt(z, c, b);
+            kw_frac(z, b, c, f);
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
               const float2 t = kw_fma2(make_float2(f[2 * h], f[2 * h + 1]), make_float2(ratio, ratio),
@@ -1024,7 +1026,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
             }
           }
           *reinterpret_cast<uint2*>(erow + 8 * j) = kw_pack_shift(be, ce.F);
-          flag = mflag || kw_minfrac(be, ce.fm) <= ce.W2;
+          flag = kw_minfrac(be, ce.fm) <= ce.W2;
         }
         kw_enqueue(q, qn, flag, j);
       }
