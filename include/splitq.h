@@ -122,6 +122,8 @@ typedef struct {
   int32_t main_natural;                            /* 1: main / MAC codes in natural channel order */
   int32_t reserved;
   int64_t acc_scratch, acc_scratch_bytes;          /* split-K partial accumulators (decode-sized calls) */
+  int64_t a_main_fp4;                              /* E2M1 copy of the main codes [tokens x ld_main / 2]
+                                                      (A2 x W3 / W2 layers, prefill: kind::mxf4 GEMM; -1 if none) */
 } splitq_ws_layout_t;
 
 const char* splitq_last_error(void);

@@ -66,7 +66,7 @@ class WsLayout(C.Structure):
         "a_mac", "s_mac", "zp_mac", "lrs_mac",
         "lr_a", "k_lr",
     )] + [("code_centered_main", _i32), ("code_centered_aux", _i32), ("main_natural", _i32),
-          ("reserved", _i32), ("acc_scratch", _i64), ("acc_scratch_bytes", _i64)]
+          ("reserved", _i32), ("acc_scratch", _i64), ("acc_scratch_bytes", _i64), ("a_main_fp4", _i64)]
 
 
 class SplitqError(RuntimeError):

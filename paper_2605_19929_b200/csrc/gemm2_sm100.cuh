@@ -53,6 +53,10 @@ constexpr int G2_THREADS = 192;         // producer, MMA, 4 epilogue warps
 constexpr int G2_THREADS_PACKED = 320;  // + 4 weight-unpack warps
 constexpr int G2_CONV_WARP0 = 6;  // warps 6..9 unpack packed weights
 constexpr int G2_TMEM_COLS = 512;
+// kind::mxf4 main path: TMEM columns [G2_SF_COL, 512) hold the block scale
+// factors, every byte UE8M0 1.0 (0x7F), so A2 / W3 codes stored as E2M1
+// multiply exactly; needs 3 bn <= G2_SF_COL (bn <= 160)
+constexpr int G2_SF_COL = 496;
 constexpr int G2_SMEM_BYTES = G2_RING_BYTES + 1024 + 512;
 
 // stage geometry for a tile width: per CTA an A box (128 x 128 B), a B box
@@ -110,7 +114,14 @@ struct G2Params {
   int64_t ld_acc;
   int64_t acc_slice;    // elements per slice
   int tile_gm;          // > 0: tiles walk groups of tile_gm m-tiles, m fastest (L2 reuse of B)
+  int mxf4;             // main operands are packed E2M1 codes (kind::mxf4, unit block scales):
+                        // k_main counts bytes, the main accumulator is fp32 (exact integers)
 };
+
+// the main accumulator word of TMEM as the exact integer it holds
+__device__ __forceinline__ int g2_acc(const G2Params& p, uint32_t w) {
+  return p.mxf4 ? (int)__uint_as_float(w) : (int)w;
+}
 
 // tile index -> (m-tile, n-tile). Default: row-major (n fastest), so the
 // concurrent CTA pairs share one A row block and stream B. With tile_gm > 0
@@ -209,6 +220,15 @@ __device__ __forceinline__ void mma_i8_pair(uint32_t d, uint64_t a, uint64_t b, 
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// D (+)= A * B on packed E2M1 codes with block scale factors from TMEM
+__device__ __forceinline__ void mma_mxf4_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                              uint32_t sfa, uint32_t sfb, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %6, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%4], [%5], p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(sfa), "r"(sfb), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void mma_f16_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
@@ -324,6 +344,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (p.mxf4) {  // unit block scale factors for the E2M1 main MMAs, in both CTAs' TMEM
+    if (warp >= 2 && warp < 6) {
+      const uint32_t lanes = (uint32_t)((warp & 3) * 32) << 16;
+      tmem_st16_fill(tmem + lanes + G2_SF_COL, 0x7F7F7F7Fu);
+      tmem_wait_st();
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+  }
   if (threadIdx.x == 0) G2_STAMP(1);  // setup done (barriers, TMEM, cluster sync)
 
   if (warp == 0) {
@@ -455,9 +485,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
             const int c = v;
             const int nk = (p.k_main - c * 128 + 31) / 32;  // K = 32 int8 per MMA
             if (elect_one()) {
+              if (p.mxf4) {  // 32 bytes = 64 E2M1 codes per MMA
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                if (k < nk) mma_i8_pair(d_main, ad + 2 * k, bd + 2 * k, p.idesc_main, (v != s0) || k != 0);
+                for (int k = 0; k < 4; ++k)
+                  if (k < nk)
+                    mma_mxf4_pair(d_main, ad + 2 * k, bd + 2 * k, p.idesc_main, tmem + G2_SF_COL,
+                                  tmem + G2_SF_COL + 8, (v != s0) || k != 0);
+              } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  if (k < nk) mma_i8_pair(d_main, ad + 2 * k, bd + 2 * k, p.idesc_main, (v != s0) || k != 0);
+              }
               tc_commit_pair(&empty[stage]);
             }
           }
@@ -563,7 +601,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj) {
               if (j_ok && jj < nrem) {
-                p.acc_i32[base + (int64_t)jj * p.ld_acc] = has_main ? (int)am[jj] : 0;
+                p.acc_i32[base + (int64_t)jj * p.ld_acc] = has_main ? g2_acc(p, am[jj]) : 0;
                 if (aux_buf) p.acc_f32[base + (int64_t)jj * p.ld_acc] = has_aux ? __uint_as_float(af[jj]) : 0.f;
               }
             }
@@ -572,7 +610,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj) {
               if (j_ok && jj < nrem) {
-                reinterpret_cast<int*>(p.out)[base + (int64_t)jj * p.ldo] = (int)am[jj];
+                reinterpret_cast<int*>(p.out)[base + (int64_t)jj * p.ldo] = g2_acc(p, am[jj]);
                 if (has_aux && p.raw_aux) p.raw_aux[base + (int64_t)jj * p.ldo] = __uint_as_float(af[jj]);
               }
             }
@@ -583,7 +621,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
               const int zp_i = __shfl_sync(0xffffffffu, zp_l, jj);
               const int orow_i = __shfl_sync(0xffffffffu, orow_l, jj);
               if (j_ok && jj < nrem) {
-                const int a2 = (int)am[jj] - zp_i * cs_j;
+                const int a2 = g2_acc(p, am[jj]) - zp_i * cs_j;
                 const float v = a2 == 0 ? 0.f : s_i * sw_j * (float)a2;
                 if (!(fabsf(v) <= 65504.f) && p.err) atomicOr(p.err, 8 /*ERR_LR_RANGE*/);
                 const __half hv = __float2half_rn(v);
@@ -599,7 +637,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
               const int zp_i = __shfl_sync(0xffffffffu, zp_l, jj);
               const float rho_i = __shfl_sync(0xffffffffu, rho_l, jj);
               if (j_ok && jj < nrem) {
-                float v = s_i * sw_j * (float)((int)am[jj] - zp_i * cs_j);
+                float v = s_i * sw_j * (float)(g2_acc(p, am[jj]) - zp_i * cs_j);
                 if (has_aux) v = fmaf(rho_i * kap_j, __uint_as_float(af[jj]), v);
                 g2_store1(p, (int64_t)(n0 + c0 + jj) * p.ldo + j, v);
               }
@@ -651,7 +689,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
             for (int j = 0; j < 8; ++j) {
               const float sw = __shfl_sync(0xffffffffu, sw_l, g + j);
               const int cs = __shfl_sync(0xffffffffu, cs_l, g + j);
-              const int acc = (int)am[g + j] - zp * cs;
+              const int acc = g2_acc(p, am[g + j]) - zp * cs;
               const float v = acc == 0 ? 0.f : s_row * sw * (float)acc;
               bad |= row_ok && colg + j < p.N && !(fabsf(v) <= 65504.f);
               hv[j] = __float2half_rn(v);
@@ -684,7 +722,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
             const float sw = __shfl_sync(0xffffffffu, sw_l, j);
             const int cs = __shfl_sync(0xffffffffu, cs_l, j);
             const float kap = __shfl_sync(0xffffffffu, kap_l, j);
-            float v = s_row * sw * (float)((int)am[j] - zp * cs);
+            float v = s_row * sw * (float)(g2_acc(p, am[j]) - zp * cs);
             if (has_aux) v = fmaf(rho * kap, __uint_as_float(af[j]), v);
             y[j] = v;
           }
@@ -697,7 +735,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
             const int col = n0 + c0 + j;
             if (col < p.N) {
               const int64_t idx = so + (int64_t)row * p.ld_acc + col;
-              p.acc_i32[idx] = has_main ? (int)am[j] : 0;
+              p.acc_i32[idx] = has_main ? g2_acc(p, am[j]) : 0;
               if (aux_buf) p.acc_f32[idx] = has_aux ? __uint_as_float(af[j]) : 0.f;
             }
           }
@@ -708,7 +746,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
             const int col = n0 + c0 + j;
             if (col < p.N) {
               const int64_t idx = (int64_t)row * p.ldo + col;
-              o[idx] = (int)am[j];
+              o[idx] = g2_acc(p, am[j]);
               if (has_aux && p.raw_aux) p.raw_aux[idx] = __uint_as_float(af[j]);
             }
           }

@@ -151,6 +151,15 @@ void transpose_codes(const int8_t* q, int64_t K, int64_t N, int64_t ld, std::vec
   }
 }
 
+// E2M1 nibble of a small integer code k in [-3, 3]: |k| 0, 1, 2, 3 -> 0x0, 0x2,
+// 0x4, 0x5 (exponent / mantissa of 0, 1, 2, 3), sign in bit 3. Element 2i of a
+// K-major row sits in the low nibble of byte i (A and B alike, so the dot
+// products do not depend on the nibble order within a byte).
+uint8_t e2m1_of(int k) {
+  static const uint8_t mag[4] = {0x0, 0x2, 0x4, 0x5};
+  return (uint8_t)(mag[k < 0 ? -k : k] | (k < 0 ? 0x8 : 0x0));
+}
+
 double pow2_ceil(double v) {  // smallest power of two >= v (v > 0)
   int e;
   const double m = std::frexp(v, &e);  // v = m * 2^e, m in [0.5, 1)
@@ -178,6 +187,7 @@ struct splitq_layer_s {
   int* c_vis = nullptr; double* d_vis = nullptr;
   int8_t* b_main = nullptr; float* s_main = nullptr; int* cs_main = nullptr;
   uint8_t* bp_main = nullptr;  // packed 4-bit main weights [d_out x ld_main / 2] (W <= 4 bits)
+  uint8_t* bf4_main = nullptr; // E2M1 main weights [d_out x ld_main / 2] (A2 x W3 / W2: kind::mxf4)
   int8_t* b_us = nullptr; float* s_us = nullptr; int* cs_us = nullptr;
   int8_t* b_uc = nullptr; float* s_uc = nullptr; int* cs_uc = nullptr;
   __half* b_lr = nullptr; float* kappa = nullptr;
@@ -372,6 +382,20 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
     }
     if ((rc = L->mem.upload(&L->bp_main, bp.data(), bp.size()))) return cleanup(rc);
   }
+  // A2 activations (centred codes in [-3, 3]) against weight codes in [-3, 3]
+  // (W3 / W2): both exact in E2M1, so the prefill main GEMM can run on
+  // kind::mxf4 (2x the int8 MMA rate) with unit block scales
+  bool fits_e2m1 = act.centered && act.qmax - act.qmin <= 3 && L->ld_main % 32 == 0;
+  for (int64_t i = 0; fits_e2m1 && i < d->n_main * N; ++i) fits_e2m1 = d->q_main[i] >= -3 && d->q_main[i] <= 3;
+  if (fits_e2m1) {
+    std::vector<uint8_t> bf((size_t)N * (L->ld_main / 2), 0);
+    for (int64_t k = 0; k < d->n_main; ++k) {
+      const int64_t kk = d->c_main[k];
+      for (int64_t n = 0; n < N; ++n)
+        bf[(size_t)n * (L->ld_main / 2) + kk / 2] |= (uint8_t)(e2m1_of(d->q_main[k * N + n]) << (4 * (kk & 1)));
+    }
+    if ((rc = L->mem.upload(&L->bf4_main, bf.data(), bf.size()))) return cleanup(rc);
+  }
   if (L->k_lr) {
     // Low-rank first stage: A_lr[i, c] = (S_a[i] / rho_i) * (S_u[c] / sigma_c) * acc[i, c]
     // with sigma_c a power of two bounding |A_lr| by 2^15 (fp16-safe for any input).
@@ -545,6 +569,7 @@ int splitq_workspace_layout(splitq_layer_t L, int64_t T, splitq_ws_layout_t* o) 
     o->acc_scratch_bytes = need;
     o->acc_scratch = need ? take(need) : -1;
   }
+  o->a_main_fp4 = L->bf4_main ? take(T * L->ld_main / 2) : -1;
   o->total_bytes = off;
   o->code_centered_main = L->act.centered;
   o->main_natural = 1;
@@ -997,6 +1022,32 @@ int launch_k1(const K1Params& k, int d_in, int device, cudaStream_t stream) {
 }  // namespace
 
 namespace {
+// int8 main codes (centred, in [-3, 3]) -> packed E2M1 codes for the
+// kind::mxf4 GEMM: 16 code bytes per thread -> 8 bytes. Per 4 codes: the
+// low 3 bits of each byte index an 8-entry byte table (PRMT), then nibble
+// pairs are merged. Codes outside [-3, 3] (the don't-care bytes of outlier
+// channels and row padding, which meet zero weights) map to finite values.
+__global__ void fp4_pack_kernel(const int8_t* __restrict__ a, int64_t lda, uint8_t* __restrict__ o, int64_t ldo,
+                                int rows, int chunks) {
+  const int64_t n = (int64_t)rows * chunks;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / chunks, c = i - r * chunks;
+    const uint4 w = *reinterpret_cast<const uint4*>(a + r * lda + 16 * c);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    uint32_t h[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t t = ws[q] & 0x07070707u;
+      const uint32_t x = t | (t >> 4);
+      const uint32_t sel = (x & 0xFFu) | ((x >> 8) & 0xFF00u);
+      const uint32_t nib = __byte_perm(0x05040200u, 0x0A0C0D00u, sel);  // E2M1 of 0,1,2,3 | -3,-2,-1
+      const uint32_t y = nib | (nib >> 4);
+      h[q] = (y & 0xFFu) | ((y >> 8) & 0xFF00u);
+    }
+    *reinterpret_cast<uint2*>(o + r * ldo + 8 * c) = make_uint2(h[0] | (h[1] << 16), h[2] | (h[3] << 16));
+  }
+}
+
 int prof_record(splitq_layer_s* L, cudaStream_t stream) {
   if (L->ev_used == L->ev_pool.size()) {
     cudaEvent_t e;
@@ -1110,6 +1161,19 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
     NvtxRange r("splitq.K1");
     if ((rc = launch_k1(k, (int)L->d_in, L->device, stream))) return rc;
   }
+  // A2 x W3 / W2 prefill: the main GEMM on kind::mxf4 from an E2M1 copy of the codes
+  static const long packed_max_rows = getenv("SPLITQ_PACKED_MAX_ROWS")
+                                          ? atol(getenv("SPLITQ_PACKED_MAX_ROWS")) : 2048;
+  const bool mxf4 = L->bf4_main && W.a_main_fp4 >= 0 && !gv && !use_swap(T) && T > packed_max_rows &&
+                    !getenv("SPLITQ_NO_MXF4");
+  if (mxf4) {
+    const int chunks = (int)(L->ld_main / 16);
+    const int64_t n = T * chunks;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 8L * sm_count(L->device));
+    fp4_pack_kernel<<<blocks, 256, 0, stream>>>((const int8_t*)at(W.a_main), L->ld_main,
+                                                (uint8_t*)at(W.a_main_fp4), L->ld_main / 2, (int)T, chunks);
+    CUDA_TRY(cudaGetLastError());
+  }
   if (prof && (rc = prof_record(L, stream))) return rc;
 
   __half* lr_a = (__half*)at(W.lr_a);
@@ -1208,8 +1272,6 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   g.p.out = y;
   g.p.ldo = y_ld;
   if (raw) g.p.raw_aux = reinterpret_cast<float*>(reinterpret_cast<int*>(y) + T * y_ld);
-  static const long packed_max_rows = getenv("SPLITQ_PACKED_MAX_ROWS")
-                                          ? atol(getenv("SPLITQ_PACKED_MAX_ROWS")) : 2048;
   if (gv) {
     GvArgs a{};
     a.a = (const int8_t*)at(W.a_main);
@@ -1226,13 +1288,22 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   }
   // box rows per CTA: the A slot holds 128 rows, the B slot bn / 2; with
   // swap-AB the weights take the A slot and the token rows the B slot
+  if (mxf4) {  // E2M1 operands: K counted in bytes (64 codes per MMA); 3 bn TMEM columns + scale factors
+    g.p.bn = std::min(g.p.bn, G2_BN);
+    g.p.k_main = (int)(L->ld_main / 2);
+    g.p.mxf4 = 1;
+    g.p.idesc_main = make_idesc_mxf4(G2_BM, g.p.bn);
+  }
   const uint32_t act_box = sw ? g.p.bn / 2 : 128, w_box = sw ? 128 : g.p.bn / 2;
-  bool ok = map_i8(&g.maps.a, at(W.a_main), T, L->k_nat, L->ld_main, act_box);
+  bool ok = mxf4 ? map_i8(&g.maps.a, at(W.a_main_fp4), T, L->ld_main / 2, L->ld_main / 2, act_box)
+                 : map_i8(&g.maps.a, at(W.a_main), T, L->k_nat, L->ld_main, act_box);
   // Packed 4-bit weights pay where the GEMM streams weights (few token rows:
   // decode); for large token counts the kernel is tensor / SMEM-bandwidth
   // bound and the SMEM unpack traffic (+50% over the UMMA operand reads at
   // 256 x 128 tiles) costs more than it saves, so the int8 expansion is used.
-  if (L->bp_main && !raw_unpacked(flags) && T <= packed_max_rows) {
+  if (mxf4) {
+    ok = ok && map_i8(&g.maps.b, L->bf4_main, L->d_out, L->ld_main / 2, L->ld_main / 2, w_box);
+  } else if (L->bp_main && !raw_unpacked(flags) && T <= packed_max_rows) {
     g.p.packed_b = 1;
     ok = ok && make_map_2d(&g.maps.b, L->bp_main, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, L->d_out,
                            L->ld_main / 2, L->ld_main / 2, w_box, 64, CU_TENSOR_MAP_SWIZZLE_NONE);
