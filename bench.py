@@ -87,12 +87,12 @@ _UNIT_BYTES = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e1
 
 def ncu_gemm_traffic(path=None):
     """DRAM bytes per split-GEMM launch (dram__bytes_read.sum + write.sum) from
-    the committed `ncu --set full` capture of one bench step (profiles/r01,
+    the committed `ncu --set full` capture of one bench step (profiles/r02,
     tools/gpu_profile.sh): the mean over the captured SPLIT-mode launches
     (every third launch of the kernel: LR1 CWS, LR1 MAC, split). None if
     absent. ncu's raw page reports these in Gbyte."""
-    path = path or os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01",
-                                "ncu_gemm_r01.json")
+    path = path or os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02",
+                                "ncu_gemm_r02.json")
     try:
         ks = json.load(open(path))["kernels"]
     except (OSError, ValueError, KeyError):
@@ -596,7 +596,7 @@ def _ref_worker(i):
     g, sp, layer = st["layers"][i]
     with threadpool_limits(st["blas"]):
         t0 = time.perf_counter()
-        orc.forward(st["L"][sp.name], st["x"][g], st["tags"])
+        orc.forward(st["L"][sp.name], st["x"][g], st["tags"], with_masks=True)
         return time.perf_counter() - t0
 
 
@@ -643,7 +643,7 @@ def run_reference(args):
     sample = (f"{tokens_sample} tokens per step through all 7 projections; the projections run "
               f"concurrently in {procs} forked processes with {max(1, cores // procs)} BLAS "
               f"thread(s) each on {cores} cores (numpy fp64, including the reference's per-call "
-              "weight re-quantization)")
+              "weight re-quantization and STE clamp masks, layer.py:100-103)")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall,
