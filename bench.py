@@ -62,7 +62,7 @@ def parse():
     ap.add_argument("--wbits", type=int, default=4)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-tokens", type=int, default=512)
+    ap.add_argument("--cpu-sample-tokens", type=int, default=2048)
     ap.add_argument("--out-dtype", default="float16", choices=["float16", "bfloat16", "float32"])
     ap.add_argument("--model", default="7b", choices=["7b", "3b"],
                     help="projection shapes: Qwen2.5-VL-7B (config 3/4, the headline) or -3B (config 2)")
@@ -647,7 +647,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f64 (numpy fake-quantization, as the reference)", "data": "synthetic",
         "config": {"workload": "config3: Qwen2.5-VL-7B decoder projections q,k,v,o,gate,up,down; "
                                "W4A4, CWS+MAC on, K_t=K_v=32",
