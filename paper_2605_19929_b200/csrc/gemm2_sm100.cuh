@@ -57,7 +57,8 @@ constexpr int G2_TMEM_COLS = 512;
 // factors, every byte UE8M0 1.0 (0x7F), so A2 / W3 codes stored as E2M1
 // multiply exactly; needs 3 bn <= G2_SF_COL (bn <= 160)
 constexpr int G2_SF_COL = 496;
-constexpr int G2_SMEM_BYTES = G2_RING_BYTES + 1024 + 512;
+constexpr int G2_COLC_BYTES = 2048;        // per-tile column constants of the fast epilogue
+constexpr int G2_SMEM_BYTES = G2_RING_BYTES + 1024 + 512 + G2_COLC_BYTES;
 
 // stage geometry for a tile width: per CTA an A box (128 x 128 B), a B box
 // (bn/2 x 128 B) and, with packed weights, the packed staging box (bn/2 x 64 B)
@@ -116,7 +117,27 @@ struct G2Params {
   int tile_gm;          // > 0: tiles walk groups of tile_gm m-tiles, m fastest (L2 reuse of B)
   int mxf4;             // main operands are packed E2M1 codes (kind::mxf4, unit block scales):
                         // k_main counts bytes, the main accumulator is fp32 (exact integers)
+  int epi_fast;         // SPLIT epilogue without zero points and with |acc| < 2^22 (or mxf4): column
+                        // constants from SMEM, packed fp32 math, exact magic-number int -> float
 };
+
+__device__ __forceinline__ uint64_t g2_pk(float2 a) { return *reinterpret_cast<uint64_t*>(&a); }
+__device__ __forceinline__ float2 g2_upk(uint64_t a) { return *reinterpret_cast<float2*>(&a); }
+__device__ __forceinline__ float2 g2_mul2(float2 a, float2 b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(g2_pk(a)), "l"(g2_pk(b)));
+  return g2_upk(r);
+}
+__device__ __forceinline__ float2 g2_add2(float2 a, float2 b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(g2_pk(a)), "l"(g2_pk(b)));
+  return g2_upk(r);
+}
+__device__ __forceinline__ float2 g2_fma2(float2 a, float2 b, float2 c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(g2_pk(a)), "l"(g2_pk(b)), "l"(g2_pk(c)));
+  return g2_upk(r);
+}
 
 // the main accumulator word of TMEM as the exact integer it holds
 __device__ __forceinline__ int g2_acc(const G2Params& p, uint32_t w) {
@@ -291,6 +312,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
   uint64_t* tempty = tfull + 2;          // [2]
   uint64_t* aempty = tempty + 2;         // [1] aux accumulator drained by the epilogue
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
+  // fast epilogue: the tile's column constants, float4 per column pair
+  // {sw_2i, sw_2i+1, kappa_2i, kappa_2i+1}
+  float* colc = reinterpret_cast<float*>(smem + G2_RING_BYTES + 512);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -667,6 +691,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
       const uint32_t lane_base = tmem + ((uint32_t)(lq * 32) << 16) + b * p.bn;
       const uint32_t lane_aux = tmem + ((uint32_t)(lq * 32) << 16) + 2 * p.bn;
       const int orow = row_ok && p.row_map ? p.row_map[row] : row;  // LR1 destination row
+      const bool fast = p.mode == G2_SPLIT && p.epi_fast;
+      if (fast) {  // the 4 epilogue warps of this CTA stage the tile's column constants
+        asm volatile("bar.sync 2, 128;" ::: "memory");  // previous tile's readers are done
+        for (int c = r_local; c < p.bn; c += 128) {
+          const int col = n0 + c;
+          const bool ok = col < p.N;
+          float* q = colc + 4 * (c >> 1) + (c & 1);
+          q[0] = ok ? p.col_s[col] : 0.f;
+          q[2] = ok && has_aux ? p.col_kappa[col] : 0.f;
+        }
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+      }
       for (int c0 = 0; c0 < p.bn; c0 += 32) {
         uint32_t am[32], af[32];
         tmem_ld32(lane_base + c0, am);
@@ -712,7 +748,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
           continue;
         }
         float y[32];
-        if (p.mode == G2_SPLIT) {  // g2_epi_split, column constants broadcast from one load per lane
+        if (fast) {  // g2_epi_split in the same rounding order: (s_row * sw) * acc, fma(rho * kappa, aux, .)
+          const float4* cc = reinterpret_cast<const float4*>(colc) + (c0 >> 1);
+          const float2 s2 = make_float2(s_row, s_row), r2 = make_float2(rho, rho);
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const float4 k4 = cc[j >> 1];
+            float2 a2;
+            if (p.mxf4) {
+              a2 = make_float2(__uint_as_float(am[j]), __uint_as_float(am[j + 1]));
+            } else {  // |acc| < 2^22: 1.5 * 2^23 + acc is exact, and so is the subtraction
+              a2 = g2_add2(make_float2(__int_as_float((int)am[j] + 0x4B400000),
+                                       __int_as_float((int)am[j + 1] + 0x4B400000)),
+                           make_float2(-12582912.f, -12582912.f));
+            }
+            float2 v = g2_mul2(g2_mul2(s2, make_float2(k4.x, k4.y)), a2);
+            if (has_aux)
+              v = g2_fma2(g2_mul2(r2, make_float2(k4.z, k4.w)),
+                          make_float2(__uint_as_float(af[j]), __uint_as_float(af[j + 1])), v);
+            y[j] = v.x;
+            y[j + 1] = v.y;
+          }
+        } else if (p.mode == G2_SPLIT) {  // g2_epi_split, column constants broadcast from one load per lane
           const int cl = min(n0 + c0 + lane, p.N - 1);
           const float sw_l = p.col_s[cl];
           const int cs_l = p.row_zp ? p.col_cs[cl] : 0;

@@ -188,6 +188,7 @@ struct splitq_layer_s {
   int8_t* b_main = nullptr; float* s_main = nullptr; int* cs_main = nullptr;
   uint8_t* bp_main = nullptr;  // packed 4-bit main weights [d_out x ld_main / 2] (W <= 4 bits)
   uint8_t* bf4_main = nullptr; // E2M1 main weights [d_out x ld_main / 2] (A2 x W3 / W2: kind::mxf4)
+  int wmax = 0;                // max |main weight code| (bounds the int32 main accumulator)
   int8_t* b_us = nullptr; float* s_us = nullptr; int* cs_us = nullptr;
   int8_t* b_uc = nullptr; float* s_uc = nullptr; int* cs_uc = nullptr;
   __half* b_lr = nullptr; float* kappa = nullptr;
@@ -361,6 +362,7 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
   if ((rc = pack_weight(L, d->q_main, d->s_main, d->n_main, N, L->ld_main, &L->b_main, &L->s_main,
                         &L->cs_main, 1.0, nullptr, d->c_main)))
     return cleanup(rc);
+  for (int64_t i = 0; i < d->n_main * N; ++i) L->wmax = std::max(L->wmax, std::abs((int)d->q_main[i]));
   // centred codes must also fit signed 4 bits; packed rows are 16-byte multiples
   bool fits4 = wsp.qmax - wsp.qmin <= 15 && L->ld_main % 32 == 0;
   for (int64_t i = 0; fits4 && i < d->n_main * N; ++i) fits4 = d->q_main[i] >= -8 && d->q_main[i] <= 7;
@@ -1271,6 +1273,10 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   g.p.col_kappa = L->kappa;
   g.p.out = y;
   g.p.ldo = y_ld;
+  // the fast epilogue: centred codes (no zero-point term) and |acc| < 2^22,
+  // bounded by K x (q_max - q_min) x max |w| (or exact fp32 sums from mxf4)
+  g.p.epi_fast = !raw && L->act.centered && !getenv("SPLITQ_EPI_SLOW") &&
+                 (mxf4 || (double)L->ld_main * (double)(L->act.qmax - L->act.qmin) * (double)L->wmax < 4194304.0);
   if (raw) g.p.raw_aux = reinterpret_cast<float*>(reinterpret_cast<int*>(y) + T * y_ld);
   if (gv) {
     GvArgs a{};

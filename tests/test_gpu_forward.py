@@ -359,3 +359,23 @@ def test_packed_cache_sees_inplace_edits():
     assert runtime.packed(layer) is g1
     layer.branch_smooth.gate[0] *= 0.5
     assert runtime.packed(layer) is not g1
+
+
+@pytest.mark.parametrize("name", ["c1_small", "no_lowrank", "no_outliers", "f16_input", "wide_n", "k110_down",
+                                  "sym_a4", "a3w3"])
+@pytest.mark.parametrize("dt", ["float32", "float16"])
+def test_fast_epilogue_bit_identical(name, dt, monkeypatch):
+    """The split GEMM's fast epilogue (column constants from SMEM, packed
+    fp32 math, magic-number int -> float) keeps the slow epilogue's rounding
+    order: outputs bit-identical (SPLITQ_EPI_SLOW=1 selects the slow one)."""
+    from paper_2605_19929_b200 import runtime
+    c = dict(CASES[name])
+    c["T"] = max(c["T"], 2100)  # the tcgen05 prefill path
+    layer, x, tags = _case(**c)
+    g = runtime.packed(layer)
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    td = torch.from_numpy(tags).cuda()
+    a = g.run(xd, td, out_dtype=getattr(torch, dt)).cpu().numpy()
+    monkeypatch.setenv("SPLITQ_EPI_SLOW", "1")
+    b = g.run(xd, td, out_dtype=getattr(torch, dt)).cpu().numpy()
+    np.testing.assert_array_equal(a, b)
