@@ -301,16 +301,24 @@ __device__ __forceinline__ float kw_x(const T* xrow, int c) {
   return XW<T>::to_f2((uint32_t)h).x;
 }
 
+// fp64 smoothing factor of channel c: from the global table, or from the
+// row group's SMEM copy (KwD::smem)
+struct KwD {
+  const double* d;
+  bool smem;
+  __device__ __forceinline__ double operator[](int c) const { return smem ? d[c] : __ldg(d + c); }
+};
+
 // exact main code of channel c: returns q, writes z64
-__device__ __forceinline__ int kw_exact_main(const K1Params& p, float x, int c, const KwRow& r,
+__device__ __forceinline__ int kw_exact_main(const K1Params& p, const KwD& dm, float x, int c, const KwRow& r,
                                              double& z64) {
-  z64 = __dmul_rn((double)x, __ldg(p.d_main + c));
+  z64 = __dmul_rn((double)x, dm[c]);
   return kw_exact_code(z64, r.S, r.zp, p.act.qmin, p.act.qmax);
 }
 // exact MAC residual e64 of channel c (layer.py:135-136, 157-159)
-__device__ __forceinline__ double kw_exact_e(const K1Params& p, float x, int c, const KwRow& r) {
+__device__ __forceinline__ double kw_exact_e(const K1Params& p, const KwD& dm, float x, int c, const KwRow& r) {
   double z64;
-  const int q = kw_exact_main(p, x, c, r, z64);
+  const int q = kw_exact_main(p, dm, x, c, r, z64);
   return __dsub_rn(z64, __dmul_rn((double)(q - r.zp), r.S));
 }
 
@@ -372,6 +380,9 @@ __device__ __forceinline__ float kw_unfkey64(uint64_t k) {
   const int i = (int)((uint32_t)k ^ 0x80000000u);
   return __int_as_float(i ^ ((i >> 31) & 0x7FFFFFFF));
 }
+// row groups stage the fp64 smoothing factors in SMEM for rows up to 8192
+// channels (14 B per channel with the x row and the fp32 factors)
+__host__ __device__ constexpr bool kw_stage64(int d_in) { return d_in <= 8192; }
 constexpr int KW_RED_SITES = 6;  // SMEM key blocks per row group: sites x WPR x 8 keys
 
 // compute_params (quantizer.py:118-135) returning 1 / S as well
@@ -526,6 +537,24 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
   // pass A; the later passes read them there
   uint4* xs = reinterpret_cast<uint4*>(red + KW_RED_SITES * WPR * 8 + 2);
   float4* ds = reinterpret_cast<float4*>(xs + nchunks);
+  // ... and, for rows up to 8192 channels, the fp64 smoothing factors too, so
+  // the exact paths (band candidates, flagged chunks, MAC residuals) read
+  // SMEM instead of making global round trips on the row's critical path
+  // (one bulk copy per CTA, issued before the first row and awaited just
+  // before the first exact path)
+  double* d64s = reinterpret_cast<double*>(ds + 2 * nchunks);
+  uint64_t* d64bar = red + KW_RED_SITES * WPR * 8 + 1;
+  const bool st64 = WPR > 1 && kw_stage64(d_in) && ((reinterpret_cast<uintptr_t>(p.d_main) & 15) == 0);
+  const KwD dm{st64 ? d64s : p.d_main, st64};
+  if (st64 && threadIdx.x == 0) {
+    mbar_init(d64bar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(d64bar, (uint32_t)d_in * 8u);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(d64s)),
+                 "l"(p.d_main), "r"((uint32_t)d_in * 8u), "r"(smem_u32(d64bar))
+                 : "memory");
+  }
   [[maybe_unused]] const int gw = WPR > 1 ? (int)blockIdx.x : (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nw = WPR > 1 ? (int)gridDim.x : (int)((gridDim.x * blockDim.x) >> 5);
   const bool cen = p.act.centered != 0, cena = p.aux.centered != 0;
@@ -567,6 +596,10 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
     uint32_t nm = 0u;
     KwRaw pa{};
     if (PF && gl < nchunks) pa = kw_ldraw(p, xg, gl);
+    // row groups: the outlier channels' x is gathered with the first chunk's
+    // loads (its latency hides under pass A, not after it)
+    uint16_t hx_t = 0, hx_v = 0;
+    bool gathered = false;
     for (int j = gl; j < nchunks; j += GT) {
       uint4 w;
       float4 da, db;
@@ -579,6 +612,11 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
         db = __ldg(reinterpret_cast<const float4*>(p.d_main32) + 2 * j + 1);
       }
       if constexpr (WPR > 1) {
+        if (!gathered) {
+          gathered = true;
+          if (pc_t >= 0) hx_t = __ldg(reinterpret_cast<const uint16_t*>(xrow) + pc_t);
+          if (pc_v >= 0) hx_v = __ldg(reinterpret_cast<const uint16_t*>(xrow) + pc_v);
+        }
         xs[j] = w;
         ds[j] = da;
         ds[nchunks + j] = db;
@@ -622,14 +660,18 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
     if constexpr (WPR > 1) {
       kw_outlier_ext<T>(xrow, p.c_text, p.d_text, p.n_text, tlo, thi, nan, gl + GT, GT);
       kw_outlier_ext<T>(xrow, p.c_vis, p.d_vis, p.n_vis, vlo, vhi, nan, gl + GT, GT);
+      if (!gathered) {
+        if (pc_t >= 0) hx_t = __ldg(reinterpret_cast<const uint16_t*>(xrow) + pc_t);
+        if (pc_v >= 0) hx_v = __ldg(reinterpret_cast<const uint16_t*>(xrow) + pc_v);
+      }
       if (pc_t >= 0) {
-        const double z = __dmul_rn((double)kw_x<T>(xrow, pc_t), pd_t);
+        const double z = __dmul_rn((double)XW<T>::to_f2((uint32_t)hx_t).x, pd_t);
         nan |= z != z;
         tlo = fmin(tlo, z);
         thi = fmax(thi, z);
       }
       if (pc_v >= 0) {
-        const double z = __dmul_rn((double)kw_x<T>(xrow, pc_v), pd_v);
+        const double z = __dmul_rn((double)XW<T>::to_f2((uint32_t)hx_v).x, pd_v);
         nan |= z != z;
         vlo = fmin(vlo, z);
         vhi = fmax(vhi, z);
@@ -674,6 +716,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
       continue;
     }
 
+    if (dm.smem) mbar_wait(d64bar, 0);  // the staged fp64 factors (first row of the CTA)
     // ------------------------------------------------ exact main extremes: candidates
     // are the elements within 2^-21 of the fp32 extremes (one chunk per lane, or all
     // of the lane's chunks when its second-best chunk is also in the band)
@@ -690,8 +733,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
         for (int u = 0; u < 8; ++u) {
           if (z[u] <= bl || -z[u] <= bh) {
             double z64;
-            (void)kw_exact_main;
-            z64 = __dmul_rn((double)kw_x<T>(xr, 8 * j + u), __ldg(p.d_main + 8 * j + u));
+            z64 = __dmul_rn((double)kw_x<T>(xr, 8 * j + u), dm[8 * j + u]);
             if (z[u] <= bl) lo64 = fmin(lo64, z64);
             if (-z[u] <= bh) hi64 = fmax(hi64, z64);
           }
@@ -848,7 +890,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
     for (int i = allx ? gl : lane; i < nfix; i += allx ? GT : 32) {
       const int ch = 8 * (allx ? i >> 3 : (int)q[i >> 3]) + (i & 7);
       double z64;
-      const int qc = kw_exact_main(p, kw_x<T>(xr, ch), ch, r, z64);
+      const int qc = kw_exact_main(p, dm, kw_x<T>(xr, ch), ch, r, z64);
       arow[ch] = (int8_t)(cen ? qc - zp : qc);
       if (mac) {
         const double e64 = __dsub_rn(z64, __dmul_rn((double)(qc - zp), S));
@@ -885,7 +927,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           if (f[u] <= bfl || -f[u] <= bfh) {
-            const double e64 = kw_exact_e(p, kw_x<T>(xr, 8 * j + u), 8 * j + u, r);
+            const double e64 = kw_exact_e(p, dm, kw_x<T>(xr, 8 * j + u), 8 * j + u, r);
             if (f[u] <= bfl) elo64 = fmin(elo64, e64);
             if (-f[u] <= bfh) ehi64 = fmax(ehi64, e64);
           }
@@ -957,11 +999,11 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
           kwl(j, x, d);
           const uint2 cm = *reinterpret_cast<const uint2*>(arow + 8 * j);  // exact main codes (pass E + fixups)
           const uint32_t cw[2] = {cm.x, cm.y};
-          const double2* d64 = reinterpret_cast<const double2*>(p.d_main + 8 * j);
+          const double2* d64 = reinterpret_cast<const double2*>((dm.smem ? d64s : p.d_main) + 8 * j);
           uint32_t by[2] = {0u, 0u};
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
-            const double2 dd = __ldg(d64 + h);
+            const double2 dd = dm.smem ? d64[h] : __ldg(d64 + h);
 #pragma unroll
             for (int u2 = 0; u2 < 2; ++u2) {
               const int u = 2 * h + u2;
@@ -1050,7 +1092,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
     __syncwarp();
     for (int i = allg2 ? gl : lane; i < ngix; i += allg2 ? GT : 32) {
       const int ch = 8 * (allg2 ? i >> 3 : (int)q[i >> 3]) + (i & 7);
-      const double e64 = kw_exact_e(p, kw_x<T>(xr, ch), ch, r);
+      const double e64 = kw_exact_e(p, dm, kw_x<T>(xr, ch), ch, r);
       const int qe = kw_exact_code(e64, Se, zpe, p.aux.qmin, p.aux.qmax);
       erow[ch] = (int8_t)(cena ? qe - zpe : qe);
     }
@@ -1063,7 +1105,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
 
 inline size_t k1w_smem(int d_in, int warps, bool smf, int wpr = 1) {
   return (size_t)warps * (KW_QCAP * 4 + (smf ? (size_t)d_in * 2 : 0)) +
-         (wpr > 1 ? (size_t)KW_RED_SITES * wpr * 8 * 8 + 16 + (size_t)d_in * 6 : 0);
+         (wpr > 1 ? (size_t)KW_RED_SITES * wpr * 8 * 8 + 16 + (size_t)d_in * (kw_stage64(d_in) ? 14 : 6) : 0);
 }
 
 }  // namespace splitq
