@@ -45,7 +45,7 @@ constexpr int GV_MAX_ROWS = 32;  // NT <= 4 MMA n-tiles of 8 token rows
 constexpr int GV_WARPS = 8;                 // consumer (MMA) warps
 constexpr int GV_THREADS = (GV_WARPS + 1) * 32;  // + one producer (TMA) warp
 constexpr int GV_BPU = 8;         // 128-byte boxes per ring unit (16 KB stages)
-constexpr int GV_MAX_STAGES = 4;
+constexpr int GV_MAX_STAGES = 12;
 constexpr int GV_BOX_BYTES = 16 * 128;
 
 struct GvArgs {
@@ -57,6 +57,8 @@ struct GvArgs {
   int units_main, units_aux;
   int stages;
   int act_stride, aux_stride;  // SMEM row strides of the staged activations (bytes)
+  int srows;            // staged token rows (<= 8 NT): the launch's rows; the MMA's
+                        // rows past them read the last staged row (their results are dropped)
   const __half* xa;     // aux operand rows [rows x k_aux] (SPLIT / RAW)
   // K split over CTAs (LR1: few channels, long K): ksplit CTAs per channel
   // block add their int32 partials into red [rows x N] (zeroed by the
@@ -111,7 +113,6 @@ __device__ __forceinline__ void gv_bar_consumers() {  // named barrier of the 8 
 template <bool PACKED, bool ASIGNED, bool LR1, int NT>
 __device__ __forceinline__ void gv_body(const GvMaps& maps, const G2Params& p, const GvArgs& g, int blocks,
                                         int bid, int nbid) {
-  constexpr int RT = 8 * NT;  // staged token rows
   extern __shared__ __align__(16) uint8_t gv_smem[];
   __shared__ int s_acc[GV_WARPS][32][4];
   __shared__ float s_aux[GV_WARPS][32][4];
@@ -122,8 +123,8 @@ __device__ __forceinline__ void gv_body(const GvMaps& maps, const G2Params& p, c
   // ring first (1024-byte aligned for the 128-byte swizzle), then the rows
   uint8_t* ring = gv_smem + ((1024u - (smem_u32(gv_smem) & 1023u)) & 1023u);
   uint8_t* sact = ring + S * GV_BPU * GV_BOX_BYTES;
-  uint8_t* saux = sact + RT * g.act_stride;
-  uint64_t* full = reinterpret_cast<uint64_t*>(saux + RT * g.aux_stride);
+  uint8_t* saux = sact + g.srows * g.act_stride;
+  uint64_t* full = reinterpret_cast<uint64_t*>(saux + g.srows * g.aux_stride);
   uint64_t* empty = full + GV_MAX_STAGES;
   // units: main boxes first, then aux boxes; a K split takes a contiguous
   // range of the main units (LR1 only: no aux)
@@ -181,7 +182,7 @@ __device__ __forceinline__ void gv_body(const GvMaps& maps, const G2Params& p, c
   {
     constexpr int PB = PACKED ? 32 : 16;  // activation bytes per weight chunk
     const int pieces = g.nbox * 8;
-    for (int i = threadIdx.x; i < RT * pieces; i += CT) {
+    for (int i = threadIdx.x; i < g.srows * pieces; i += CT) {
       const int t = i / pieces, pc = i - t * pieces;
       const int b = pc >> 3, c = pc & 7;
       const int64_t src = (int64_t)(b * 8 + c) * PB;
@@ -197,7 +198,7 @@ __device__ __forceinline__ void gv_body(const GvMaps& maps, const G2Params& p, c
     }
     if (!LR1) {
       const int xp = g.nbox_aux * 8;  // 16-byte pieces
-      for (int i = threadIdx.x; i < RT * xp; i += CT) {
+      for (int i = threadIdx.x; i < g.srows * xp; i += CT) {
         const int t = i / max(xp, 1), pc = i - t * xp;
         const int b = pc >> 3, c = pc & 7;
         uint4 v = make_uint4(0, 0, 0, 0);
@@ -224,8 +225,15 @@ __device__ __forceinline__ void gv_body(const GvMaps& maps, const G2Params& p, c
     }
   gv_bar_consumers();  // staged rows visible
 
-  const uint8_t* arow = sact + gq * g.act_stride;  // this thread's B-operand token row
-  const uint8_t* xrow = saux + gq * g.aux_stride;
+  // this thread's B-operand token rows 8 j + gq (clamped to the staged rows)
+  const uint8_t* arow[NT];
+  const uint8_t* xrow[NT];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    const int r = min(8 * j + gq, g.srows - 1);
+    arow[j] = sact + r * g.act_stride;
+    xrow[j] = saux + r * g.aux_stride;
+  }
   int li = 0;
   for (int item = bid; item < items; item += nbid) {
     const int cb = item / ks_n;
@@ -276,7 +284,7 @@ __device__ __forceinline__ void gv_body(const GvMaps& maps, const G2Params& p, c
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
             const uint4* ap =
-                reinterpret_cast<const uint4*>(arow + 8 * j * g.act_stride + (b0 + b) * 256 + slot * 32);
+                reinterpret_cast<const uint4*>(arow[j] + (b0 + b) * 256 + slot * 32);
             const uint4 x0 = ap[0], x1 = ap[1];
             const uint32_t av[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
@@ -287,7 +295,7 @@ __device__ __forceinline__ void gv_body(const GvMaps& maps, const G2Params& p, c
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
             const uint4 x0 =
-                *reinterpret_cast<const uint4*>(arow + 8 * j * g.act_stride + (b0 + b) * 128 + slot * 16);
+                *reinterpret_cast<const uint4*>(arow[j] + (b0 + b) * 128 + slot * 16);
             gv_mma_i8<ASIGNED>(acc[j], wl.x, wh.x, wl.y, wh.y, x0.x, x0.y);
             gv_mma_i8<ASIGNED>(acc[j], wl.z, wh.z, wl.w, wh.w, x0.z, x0.w);
           }
@@ -295,7 +303,7 @@ __device__ __forceinline__ void gv_body(const GvMaps& maps, const G2Params& p, c
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
             const uint4 x0 =
-                *reinterpret_cast<const uint4*>(xrow + 8 * j * g.aux_stride + (b0 + b) * 128 + slot * 16);
+                *reinterpret_cast<const uint4*>(xrow[j] + (b0 + b) * 128 + slot * 16);
             gv_mma_f16(ax[j], wl.x, wh.x, wl.y, wh.y, x0.x, x0.y);
             gv_mma_f16(ax[j], wl.z, wh.z, wl.w, wh.w, x0.z, x0.w);
           }

@@ -702,17 +702,24 @@ inline int gv_ntiles(int64_t rows) { return rows <= 8 ? 1 : rows <= 16 ? 2 : 4; 
 
 // GEMV launch shape from the token rows, the weight row bytes and the aux K;
 // false when the staged rows leave no room for a 2-deep ring
-bool gv_shape(int64_t rows, bool packed, int64_t row_bytes, int k_aux, GvArgs* g, int* smem) {
-  const int rt = 8 * gv_ntiles(rows);
+// ctas_per_sm: CTAs each SM should hold (the launch's CTAs over the SMs):
+// the ring takes what SMEM is left for that many; deeper rings keep more
+// weight bytes in flight per SM (the GEMV streams at ring / latency)
+bool gv_shape(int64_t rows, bool packed, int64_t row_bytes, int k_aux, GvArgs* g, int* smem,
+              int ctas_per_sm = 1) {
+  g->srows = (int)std::max<int64_t>(1, std::min<int64_t>(rows, 8 * gv_ntiles(rows)));
   g->nbox = (int)((row_bytes + 127) / 128);
   g->nbox_aux = k_aux / 64;
   g->units_main = (g->nbox + GV_BPU - 1) / GV_BPU;
   g->units_aux = (g->nbox_aux + GV_BPU - 1) / GV_BPU;
   g->act_stride = packed ? g->nbox * 256 + 16 : g->nbox * 128 + 64;
   g->aux_stride = k_aux ? g->nbox_aux * 128 + 64 : 0;
-  const int fixed = gv_smem_bytes(rt, g->act_stride, g->aux_stride, 0);
-  g->stages = std::min(GV_MAX_STAGES, (kGvSmemBudget - fixed) / (GV_BPU * GV_BOX_BYTES));
-  *smem = gv_smem_bytes(rt, g->act_stride, g->aux_stride, g->stages);
+  const int fixed = gv_smem_bytes(g->srows, g->act_stride, g->aux_stride, 0);
+  const int budget = std::min(kGvSmemBudget, 227 * 1024 / std::max(ctas_per_sm, 1) - 9 * 1024);
+  g->stages = std::min(GV_MAX_STAGES, (budget - fixed) / (GV_BPU * GV_BOX_BYTES));
+  if (g->stages < 2)  // too many CTAs per SM asked for: the largest ring one CTA fits
+    g->stages = std::min(GV_MAX_STAGES, (kGvSmemBudget - fixed) / (GV_BPU * GV_BOX_BYTES));
+  *smem = gv_smem_bytes(g->srows, g->act_stride, g->aux_stride, g->stages);
   return g->stages >= 2;
 }
 
@@ -785,6 +792,10 @@ int gv_plan(GvPlan& pl, const G2Params& p, const GvArgs& g, int rows, const void
   pl.g.ksplit = 1;
   if (lr1 && pl.g.red)
     pl.g.ksplit = std::max(1, std::min(pl.g.units_main, sm_count(device) / std::max(pl.blocks, 1)));
+  // more CTAs than SMs: size the ring so that up to 2 fit an SM
+  const int per_sm = std::min(2, (pl.blocks * pl.g.ksplit + sm_count(device) - 1) / sm_count(device));
+  if (per_sm > 1 && !gv_shape(rows, packed, row_bytes, k_aux, &pl.g, &pl.smem, per_sm))
+    return fail(SPLITQ_ERR_UNSUPPORTED, "GEMV shape");
   bool ok = make_map_2d(&pl.maps.w, w, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, p.N, row_bytes, row_bytes, 16, 128);
   pl.maps.x = pl.maps.w;
   if (ok && k_aux)
