@@ -788,10 +788,17 @@ int gv_plan(GvPlan& pl, const G2Params& p, const GvArgs& g, int rows, const void
   const int k_aux = lr1 ? 0 : p.k_aux;
   if (!gv_shape(rows, packed, row_bytes, k_aux, &pl.g, &pl.smem)) return fail(SPLITQ_ERR_UNSUPPORTED, "GEMV shape");
   pl.blocks = (p.N + 15) / 16;
-  // LR1 (few channel blocks, long K): split K over CTAs so ~one CTA per SM streams
+  // LR1 (few channel blocks, long K): split K over CTAs only as far as one
+  // CTA's ring cannot hold its range (a split adds the integer atomics, the
+  // arrival counter and the read-back to the chain; a ring-sized range is one
+  // round trip). SPLITQ_GV_KSPLIT (read per call, tests) forces the split.
   pl.g.ksplit = 1;
-  if (lr1 && pl.g.red)
-    pl.g.ksplit = std::max(1, std::min(pl.g.units_main, sm_count(device) / std::max(pl.blocks, 1)));
+  if (lr1 && pl.g.red) {
+    const char* e = getenv("SPLITQ_GV_KSPLIT");
+    const int by_ring = (pl.g.units_main + pl.g.stages - 1) / std::max(pl.g.stages, 1);
+    pl.g.ksplit = std::max(1, std::min({e ? atoi(e) : by_ring, pl.g.units_main,
+                                        sm_count(device) / std::max(pl.blocks, 1)}));
+  }
   // more CTAs than SMs: size the ring so that up to 2 fit an SM
   const int per_sm = std::min(2, (pl.blocks * pl.g.ksplit + sm_count(device) - 1) / sm_count(device));
   if (per_sm > 1 && !gv_shape(rows, packed, row_bytes, k_aux, &pl.g, &pl.smem, per_sm))

@@ -332,6 +332,19 @@ def test_gemv_multi_tile(name, monkeypatch):
     _check_out(layer, x, tags)
 
 
+@pytest.mark.parametrize("ksplit", ["1", "3"])
+@pytest.mark.parametrize("name", ["decode_t2", "decode_t4_k4096", "decode_t16", "decode_t5_a8"])
+def test_gemv_lr1_k_split(name, ksplit, monkeypatch):
+    """The decode low-rank first stage with K split over CTAs (integer
+    atomics, last-arriving CTA applies the epilogue) and unsplit: LR1
+    outputs feed the aux operand, so the outputs and the int32 main
+    accumulators must match the oracle either way."""
+    monkeypatch.setenv("SPLITQ_GV_KSPLIT", ksplit)
+    layer, x, tags = _case(**CASES[name])
+    _check_acc(layer, x, tags)
+    _check_out(layer, x, tags)
+
+
 def test_run_validates_buffers():
     """GpuLayer.run rejects mismatched tags / outputs / devices before launching."""
     from paper_2605_19929_b200 import runtime
