@@ -655,6 +655,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
 
     // outlier paths: exact fp64 extremes (every warp of a group: few channels)
     double tlo, thi, vlo, vhi;
+    double z_t = 0.0, z_v = 0.0;  // row groups: this thread's outlier z (reused for its code)
     bool nan = XW<T>::nonfinite(nm);
     // (a row group spreads the outlier channels over all its threads)
     if constexpr (WPR > 1) {
@@ -665,16 +666,16 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
         if (pc_v >= 0) hx_v = __ldg(reinterpret_cast<const uint16_t*>(xrow) + pc_v);
       }
       if (pc_t >= 0) {
-        const double z = __dmul_rn((double)XW<T>::to_f2((uint32_t)hx_t).x, pd_t);
-        nan |= z != z;
-        tlo = fmin(tlo, z);
-        thi = fmax(thi, z);
+        z_t = __dmul_rn((double)XW<T>::to_f2((uint32_t)hx_t).x, pd_t);
+        nan |= z_t != z_t;
+        tlo = fmin(tlo, z_t);
+        thi = fmax(thi, z_t);
       }
       if (pc_v >= 0) {
-        const double z = __dmul_rn((double)XW<T>::to_f2((uint32_t)hx_v).x, pd_v);
-        nan |= z != z;
-        vlo = fmin(vlo, z);
-        vhi = fmax(vhi, z);
+        z_v = __dmul_rn((double)XW<T>::to_f2((uint32_t)hx_v).x, pd_v);
+        nan |= z_v != z_v;
+        vlo = fmin(vlo, z_v);
+        vhi = fmax(vhi, z_v);
       }
     } else {
       kw_outlier_ext<T>(xrow, p.c_text, p.d_text, p.n_text, tlo, thi, nan);
@@ -803,10 +804,10 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
     // (a row group spreads both outlier paths over all its threads)
     if (p.n_text > 0)
       outlier_codes(p, row, xr, p.c_text, p.d_text, p.n_text, p.ld_text, p.a_text, rt,
-                    rt.S * rrho, p.lr_off_t, p.kt16, WPR > 1 ? gl : -1, GT);
+                    rt.S * rrho, p.lr_off_t, p.kt16, WPR > 1 ? gl : -1, GT, pc_t >= 0 ? &z_t : nullptr);
     if (p.n_vis > 0)
       outlier_codes(p, row, xr, p.c_vis, p.d_vis, p.n_vis, p.ld_vis, p.a_vis, rv, rv.S * rrho,
-                    p.lr_off_v, p.kv16, WPR > 1 ? gl : -1, GT);
+                    p.lr_off_v, p.kv16, WPR > 1 ? gl : -1, GT, pc_v >= 0 ? &z_v : nullptr);
     if (p.k_lr > 0) {  // the low-rank columns of the aux operand row: LR1 fills them
       uint4* lr = reinterpret_cast<uint4*>(p.lr_a + (int64_t)row * p.k_lr + p.lr_off_s);
       for (int i = gl; i < (p.k_lr - p.lr_off_s) / 8; i += GT) lr[i] = make_uint4(0, 0, 0, 0);

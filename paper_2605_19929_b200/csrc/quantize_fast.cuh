@@ -156,7 +156,8 @@ __device__ void outlier_params(const K1Params& p, const T* xs, const int* cols, 
 template <typename T>
 __device__ void outlier_codes(const K1Params& p, int row, const T* xs, const int* cols,
                               const double* d, int n, int ld, int8_t* codes, const RowParams& rp,
-                              double fac, int seg_off, int k16, int k0 = -1, int step = 32) {
+                              double fac, int seg_off, int k16, int k0 = -1, int step = 32,
+                              const double* z0 = nullptr) {  // z of channel k0, if already formed
   int8_t* out = codes + (int64_t)row * ld;
   __half* seg = p.k_lr > 0 ? p.lr_a + (int64_t)row * p.k_lr + seg_off : nullptr;
   const int lim = max(ld, k16);
@@ -164,7 +165,7 @@ __device__ void outlier_codes(const K1Params& p, int row, const T* xs, const int
     int c = 0;
     double a = 0.0;
     if (k < n) {
-      const double z = __dmul_rn(to_f64(xs[cols[k]]), d[k]);
+      const double z = z0 && k == k0 ? *z0 : __dmul_rn(to_f64(xs[cols[k]]), d[k]);
       bool tie = false;
       int q = quant_row(z, rp, tie);
       if (tie) q = quant_exact(z, rp.S, 0.0, rp.zp, rp.qmin, rp.qmax);
