@@ -623,7 +623,12 @@ int launch_gemm(GemmLaunch& g, int device, int64_t max_rows, cudaStream_t stream
   const int64_t slice = max_rows * g.p.N;
   g.p.k_split = 1;
   int final_mode = g.p.mode;
-  if (scratch && tiles * 2 <= avail && stages >= 2 && !getenv("SPLITQ_NO_SPLITK")) {
+  // LR1 (N = rank, short rows of tiles): the split's scratch pass and extra
+  // launch only pay for long K or very few tiles (7B q-proj LR1 at 8192
+  // tokens: 71 us split vs 52 us unsplit; down-proj, K = 18944: split wins
+  // up to ~8192 tokens)
+  const bool split_ok = g.p.mode != G2_LR1 || stages >= 64 || tiles * 8 <= avail;
+  if (scratch && split_ok && tiles * 2 <= avail && stages >= 2 && !getenv("SPLITQ_NO_SPLITK")) {
     int ks = (int)std::min<int64_t>(stages, std::max<int64_t>(2, avail / tiles));
     while (ks > 1 && ks * slice * (has_aux ? 8 : 4) > scratch_bytes) --ks;  // slices must fit
     if (ks > 1) {
