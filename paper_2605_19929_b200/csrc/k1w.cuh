@@ -211,6 +211,24 @@ __device__ __forceinline__ void kw_cvt(const KwRaw& r, float (&x)[8], float (&d)
   d[4] = r.db.x; d[5] = r.db.y; d[6] = r.db.z; d[7] = r.db.w;
 }
 
+// x from the row group's SMEM copy, the factors from the global fp32 table
+template <typename T>
+__device__ __forceinline__ void kw_load_xs(const K1Params& p, const uint4* xs, int j, float (&x)[8],
+                                           float (&d)[8]) {
+  const uint4 w = xs[j];
+  const float4 da = __ldg(reinterpret_cast<const float4*>(p.d_main32) + 2 * j);
+  const float4 db = __ldg(reinterpret_cast<const float4*>(p.d_main32) + 2 * j + 1);
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const float2 f2 = XW<T>::to_f2(ws[h]);
+    x[2 * h] = f2.x;
+    x[2 * h + 1] = f2.y;
+  }
+  d[0] = da.x; d[1] = da.y; d[2] = da.z; d[3] = da.w;
+  d[4] = db.x; d[5] = db.y; d[6] = db.z; d[7] = db.w;
+}
+
 // the same from the row group's SMEM copy (x plane + two d planes)
 template <typename T>
 __device__ __forceinline__ void kw_load_s(const uint4* xs, const float4* ds, int nch, int j,
@@ -537,6 +555,9 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
   // pass A; the later passes read them there
   uint4* xs = reinterpret_cast<uint4*>(red + KW_RED_SITES * WPR * 8 + 2);
   float4* ds = reinterpret_cast<float4*>(xs + nchunks);
+  // (the fp32 factors are staged only when the launch asks: for wide rows
+  // with several rows per CTA the SMEM buys more co-resident rows instead)
+  const bool sd = WPR > 1 && p.kw_stage_d;
   // ... and, for rows up to 8192 channels, the fp64 smoothing factors too, so
   // the exact paths (band candidates, flagged chunks, MAC residuals) read
   // SMEM instead of making global round trips on the row's critical path
@@ -544,7 +565,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
   // before the first exact path)
   double* d64s = reinterpret_cast<double*>(ds + 2 * nchunks);
   uint64_t* d64bar = red + KW_RED_SITES * WPR * 8 + 1;
-  const bool st64 = WPR > 1 && kw_stage64(d_in) && ((reinterpret_cast<uintptr_t>(p.d_main) & 15) == 0);
+  const bool st64 = sd && kw_stage64(d_in) && ((reinterpret_cast<uintptr_t>(p.d_main) & 15) == 0);
   const KwD dm{st64 ? d64s : p.d_main, st64};
   if (st64 && threadIdx.x == 0) {
     mbar_init(d64bar, 1);
@@ -577,7 +598,10 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
     const uint4* xg = reinterpret_cast<const uint4*>(xrow);
     const T* xr = WPR > 1 ? reinterpret_cast<const T*>(xs) : xrow;  // element reads after pass A
     auto kwl = [&](int j, float (&x)[8], float (&d)[8]) {
-      if constexpr (WPR > 1) kw_load_s<T>(xs, ds, nchunks, j, x, d);
+      if constexpr (WPR > 1) {
+        if (sd) kw_load_s<T>(xs, ds, nchunks, j, x, d);
+        else kw_load_xs<T>(p, xs, j, x, d);
+      }
       else kw_load<T>(p, xg, j, x, d);
     };
 
@@ -618,8 +642,10 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
           if (pc_v >= 0) hx_v = __ldg(reinterpret_cast<const uint16_t*>(xrow) + pc_v);
         }
         xs[j] = w;
-        ds[j] = da;
-        ds[nchunks + j] = db;
+        if (sd) {
+          ds[j] = da;
+          ds[nchunks + j] = db;
+        }
       }
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
       const float d[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
@@ -1104,9 +1130,10 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
   }
 }
 
-inline size_t k1w_smem(int d_in, int warps, bool smf, int wpr = 1) {
+inline size_t k1w_smem(int d_in, int warps, bool smf, int wpr = 1, bool stage_d = true) {
+  const size_t per_ch = 2 + (stage_d ? 4 + (kw_stage64(d_in) ? 8 : 0) : 0);  // x [+ fp32 [+ fp64] factors]
   return (size_t)warps * (KW_QCAP * 4 + (smf ? (size_t)d_in * 2 : 0)) +
-         (wpr > 1 ? (size_t)KW_RED_SITES * wpr * 8 * 8 + 16 + (size_t)d_in * (kw_stage64(d_in) ? 14 : 6) : 0);
+         (wpr > 1 ? (size_t)KW_RED_SITES * wpr * 8 * 8 + 16 + (size_t)d_in * per_ch : 0);
 }
 
 }  // namespace splitq

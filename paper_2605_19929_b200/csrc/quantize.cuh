@@ -194,6 +194,7 @@ struct K1Params {
   int* mac_count;  // K1w: MAC slots are claimed with an atomic (order-free; rows independent)
   int* mac_rows;   //      mac_rows[slot] = row
   unsigned long long* trace;  // KW_TRACE builds: phase clocks of the first row of CTA 0
+  int kw_stage_d;  // K1w row groups: stage the fp32 smoothing factors in SMEM with the row
   int8_t* a_mac;
   double* s_mac;
   int* zp_mac;

@@ -941,7 +941,13 @@ unsigned long long* k1w_trace_last = nullptr;
 template <typename T, bool SMF, int WPR, bool SYNC = false, bool G64 = false, bool PF = false>
 int launch_k1w_t(const K1Params& k, int d_in, int device, cudaStream_t stream) {
   const int threads = WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : KW_THREADS;
-  const size_t smem = k1w_smem(d_in, threads / 32, SMF, WPR);
+  // row groups stage the fp32 factors with the row for decode-sized calls
+  // and rows up to 8192 channels; wide rows with many rows per CTA keep the
+  // SMEM for co-resident row groups (SPLITQ_K1_STAGE_D=0|1 overrides)
+  K1Params kk = k;
+  const char* sde = getenv("SPLITQ_K1_STAGE_D");
+  kk.kw_stage_d = sde ? atoi(sde) : (d_in <= 8192 || k.T <= 2 * sm_count(device));
+  const size_t smem = k1w_smem(d_in, threads / 32, SMF, WPR, kk.kw_stage_d != 0);
   static int attr_dev[64] = {0};
   if (device >= 0 && device < 64 && !attr_dev[device]) {
     CUDA_TRY(cudaFuncSetAttribute(k1w_kernel<T, SMF, WPR, SYNC, G64, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -962,13 +968,10 @@ int launch_k1w_t(const K1Params& k, int d_in, int device, cudaStream_t stream) {
   static unsigned long long* kw_trace_buf = nullptr;
   if (!kw_trace_buf) cudaMalloc(&kw_trace_buf, 16 * 8);
   cudaMemsetAsync(kw_trace_buf, 0, 16 * 8, stream);
-  K1Params kt = k;
-  kt.trace = kw_trace_buf;
+  kk.trace = kw_trace_buf;
   k1w_trace_last = kw_trace_buf;
-  k1w_kernel<T, SMF, WPR, SYNC, G64, PF><<<(unsigned)grid, threads, smem, stream>>>(kt, d_in);
-#else
-  k1w_kernel<T, SMF, WPR, SYNC, G64, PF><<<(unsigned)grid, threads, smem, stream>>>(k, d_in);
 #endif
+  k1w_kernel<T, SMF, WPR, SYNC, G64, PF><<<(unsigned)grid, threads, smem, stream>>>(kk, d_in);
   CUDA_TRY(cudaGetLastError());
   return SPLITQ_OK;
 }
@@ -986,13 +989,15 @@ int launch_k1w_g(const K1Params& k, int d_in, int device, cudaStream_t stream) {
   // save). SPLITQ_K1_WPR=1|8|16 overrides.
   const char* wenv = getenv("SPLITQ_K1_WPR");  // read per call: tests switch it
   const int wpr_env = wenv ? atoi(wenv) : 0;
-  // row groups also for wide rows (d_in > 8192) when the warp-per-row launch
-  // would give each warp at most one row: one warp's serial passes over a
-  // wide row are then the critical path (3B down, d_in 11008, 4096 rows:
-  // 343 -> 147 us); from ~2 rows per warp on, warp rows win (7B down at
-  // 8192 rows: 789 vs 980 us)
+  // row groups also for wide rows (d_in > 8192) up to ~256 rows per SM: one
+  // warp's serial passes over a wide row are the critical path when each
+  // warp gets few rows, and row groups that keep only the row in SMEM (the
+  // factors from the global table, launch_k1w_t) fit 5 per SM. 7B down
+  // (d_in 18944): 4096 rows 0.53 (warp rows) -> 0.25 ms, 8192 rows 0.81 ->
+  // 0.45 ms, 16384 1.16 -> 0.88 ms, 32768 1.82 -> 1.74 ms; at 65536 warp
+  // rows win (3.04 vs 3.45 ms)
   const bool grouped = wpr_env ? wpr_env > 1
-                               : k.T <= 2 * sm_count(device) || (d_in > 8192 && k.T <= 32 * sm_count(device));
+                               : k.T <= 2 * sm_count(device) || (d_in > 8192 && k.T <= 256 * sm_count(device));
   if (grouped && !smf)
     return wpr_env >= 16 ? launch_k1w_t<T, false, 16, false, G64>(k, d_in, device, stream)  // measured slower
                          : launch_k1w_t<T, false, 8, false, G64>(k, d_in, device, stream);

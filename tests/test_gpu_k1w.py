@@ -119,17 +119,22 @@ SHAPES = {
 }
 
 
-@pytest.fixture(params=[("1", "0", "0"), ("1", "0", "1"), ("1", "1", "0"), ("8", "0", "0"), ("16", "0", "0")],
-                ids=["warp_rows", "warp_rows_prefetch", "warp_rows_sync", "cta8_rows", "cta16_rows"],
+@pytest.fixture(params=[("1", "0", "0", "1"), ("1", "0", "1", "1"), ("1", "1", "0", "1"), ("8", "0", "0", "1"),
+                        ("8", "0", "0", "0"), ("16", "0", "0", "1")],
+                ids=["warp_rows", "warp_rows_prefetch", "warp_rows_sync", "cta8_rows", "cta8_rows_global_d",
+                     "cta16_rows"],
                 autouse=True)
 def k1_row_group(request, monkeypatch):
     """Every case runs with one warp per row (prefill; plain, with loads one
     chunk ahead, with the per-round CTA barrier) and with 8- / 16-warp row
-    groups (decode-sized calls); the library reads SPLITQ_K1_WPR / _SYNC /
-    _PF per call."""
+    groups (decode-sized calls; the smoothing factors staged in SMEM with
+    the row, or read from the global table as for wide rows with many rows
+    per CTA); the library reads SPLITQ_K1_WPR / _SYNC / _PF / _STAGE_D per
+    call."""
     monkeypatch.setenv("SPLITQ_K1_WPR", request.param[0])
     monkeypatch.setenv("SPLITQ_K1_SYNC", request.param[1])
     monkeypatch.setenv("SPLITQ_K1_PF", request.param[2])
+    monkeypatch.setenv("SPLITQ_K1_STAGE_D", request.param[3])
 
 
 @pytest.mark.parametrize("dt", DTS, ids=["f16", "bf16"])
