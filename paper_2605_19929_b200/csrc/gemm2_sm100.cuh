@@ -678,9 +678,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
       }
       const int row = m0 + r_local;
       const bool row_ok = row < M;
-      mbar_wait(&tfull[b], tph);
-      tc_fence_after();
-      if (warp == 2 && lane == 0 && it == 0) G2_STAMP(6);  // accumulator ready
+      // the tile's row and column constants do not depend on the accumulator:
+      // loaded before the wait, so their latency hides under the MMAs (a
+      // tile's epilogue is on the critical path for one-tile launches: LR1,
+      // small calls, every CTA's last tile)
       float s_row = 0.f, rho = 0.f;
       int zp = 0;
       if (row_ok) {
@@ -688,10 +689,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
         if (p.row_zp) zp = p.row_zp[row];
         if (has_aux && p.row_rho) rho = p.row_rho[row];
       }
-      const uint32_t lane_base = tmem + ((uint32_t)(lq * 32) << 16) + b * p.bn;
-      const uint32_t lane_aux = tmem + ((uint32_t)(lq * 32) << 16) + 2 * p.bn;
       const int orow = row_ok && p.row_map ? p.row_map[row] : row;  // LR1 destination row
       const bool fast = p.mode == G2_SPLIT && p.epi_fast;
+      if (p.mode == G2_LR1) {  // the tile's column constants: sw [0, bn), cs [256, 256 + bn)
+        asm volatile("bar.sync 2, 128;" ::: "memory");  // previous tile's readers are done
+        for (int c = r_local; c < p.bn; c += 128) {
+          const int col = n0 + c;
+          const bool ok = col < p.N;
+          colc[c] = ok ? p.col_s[col] : 0.f;
+          reinterpret_cast<int*>(colc)[256 + c] = ok && p.row_zp ? p.col_cs[col] : 0;
+        }
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+      }
       if (fast) {  // the 4 epilogue warps of this CTA stage the tile's column constants
         asm volatile("bar.sync 2, 128;" ::: "memory");  // previous tile's readers are done
         for (int c = r_local; c < p.bn; c += 128) {
@@ -703,45 +712,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PACKED ? G2_THREADS_
         }
         asm volatile("bar.sync 2, 128;" ::: "memory");
       }
+      mbar_wait(&tfull[b], tph);
+      tc_fence_after();
+      if (warp == 2 && lane == 0 && it == 0) G2_STAMP(6);  // accumulator ready
+      const uint32_t lane_base = tmem + ((uint32_t)(lq * 32) << 16) + b * p.bn;
+      const uint32_t lane_aux = tmem + ((uint32_t)(lq * 32) << 16) + 2 * p.bn;
       for (int c0 = 0; c0 < p.bn; c0 += 32) {
         uint32_t am[32], af[32];
         tmem_ld32(lane_base + c0, am);
         if (has_aux) tmem_ld32(lane_aux + c0, af);
         tmem_wait_ld();
+        if (warp == 2 && lane == 0 && it == 0 && c0 == 0) G2_STAMP(7);  // first TMEM chunk in registers
         if (p.mode == G2_LR1) {
-          // the chunk's 32 column constants: one load per lane, broadcast by
-          // shuffles (all lanes take part; rows past M only skip the stores)
-          const int cl = n0 + c0 + lane;
-          const float sw_l = cl < p.N ? p.col_s[cl] : 0.f;
-          const int cs_l = cl < p.N && p.row_zp ? p.col_cs[cl] : 0;
+          // g2_epi_lr1 in the same rounding order, two columns at a time:
+          // v = acc == 0 ? 0 : (s_row * sw) * acc, hi = fp16(v), lo = fp16(v - hi);
+          // column constants from SMEM (broadcast reads)
           __half* o = reinterpret_cast<__half*>(p.out) + (int64_t)orow * p.ldo + p.col_off;
           const bool vec = ((p.ldo | p.col_off | p.lo_off) & 7) == 0;
+          const float2 s2 = make_float2(s_row, s_row);
 #pragma unroll
           for (int g = 0; g < 32; g += 8) {
             const int colg = n0 + c0 + g;
-            __half hv[8], lv[8];
+            const float4 swa = *reinterpret_cast<const float4*>(colc + c0 + g);
+            const float4 swb = *reinterpret_cast<const float4*>(colc + c0 + g + 4);
+            const float sw[8] = {swa.x, swa.y, swa.z, swa.w, swb.x, swb.y, swb.z, swb.w};
+            int cs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            if (p.row_zp) {
+              const int4 ca = *reinterpret_cast<const int4*>(reinterpret_cast<const int*>(colc) + 256 + c0 + g);
+              const int4 cb = *reinterpret_cast<const int4*>(reinterpret_cast<const int*>(colc) + 256 + c0 + g + 4);
+              cs[0] = ca.x; cs[1] = ca.y; cs[2] = ca.z; cs[3] = ca.w;
+              cs[4] = cb.x; cs[5] = cb.y; cs[6] = cb.z; cs[7] = cb.w;
+            }
+            __half2 hv[4], lv[4];
             bool bad = false;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float sw = __shfl_sync(0xffffffffu, sw_l, g + j);
-              const int cs = __shfl_sync(0xffffffffu, cs_l, g + j);
-              const int acc = g2_acc(p, am[g + j]) - zp * cs;
-              const float v = acc == 0 ? 0.f : s_row * sw * (float)acc;
-              bad |= row_ok && colg + j < p.N && !(fabsf(v) <= 65504.f);
-              hv[j] = __float2half_rn(v);
-              lv[j] = __float2half_rn(v - __half2float(hv[j]));
+            for (int j = 0; j < 8; j += 2) {
+              const int a0 = g2_acc(p, am[g + j]) - zp * cs[j];
+              const int a1 = g2_acc(p, am[g + j + 1]) - zp * cs[j + 1];
+              float2 v = g2_mul2(g2_mul2(s2, make_float2(sw[j], sw[j + 1])),
+                                 make_float2((float)a0, (float)a1));
+              if (a0 == 0) v.x = 0.f;
+              if (a1 == 0) v.y = 0.f;
+              bad |= !(fabsf(v.x) <= 65504.f) || !(fabsf(v.y) <= 65504.f);
+              const __half2 h = __floats2half2_rn(v.x, v.y);
+              const float2 hf = __half22float2(h);
+              const float2 r = g2_add2(v, make_float2(-hf.x, -hf.y));
+              hv[j >> 1] = h;
+              lv[j >> 1] = __floats2half2_rn(r.x, r.y);
             }
-            if (bad && p.err) atomicOr(p.err, 8 /*ERR_LR_RANGE*/);
+            bad = bad && row_ok;
+            if (bad) {  // (columns past N are zero: never bad)
+              if (p.err) atomicOr(p.err, 8 /*ERR_LR_RANGE*/);
+            }
             if (!row_ok) continue;
             if (vec && colg + 8 <= p.N) {  // 8 columns -> one 16-byte store (+ one for lo)
               *reinterpret_cast<uint4*>(o + colg) = *reinterpret_cast<const uint4*>(hv);
               if (p.lo_off) *reinterpret_cast<uint4*>(o + p.lo_off + colg) = *reinterpret_cast<const uint4*>(lv);
             } else {
+              const __half* hs = reinterpret_cast<const __half*>(hv);
+              const __half* ls = reinterpret_cast<const __half*>(lv);
 #pragma unroll
               for (int j = 0; j < 8; ++j)
                 if (colg + j < p.N) {
-                  o[colg + j] = hv[j];
-                  if (p.lo_off) o[p.lo_off + colg + j] = lv[j];
+                  o[colg + j] = hs[j];
+                  if (p.lo_off) o[p.lo_off + colg + j] = ls[j];
                 }
             }
           }
