@@ -195,6 +195,10 @@ struct splitq_layer_s {
   // stage timing (SPLITQ_FWD_PROFILE): 4 events per profiled call
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
+  // prefill: the MAC first stage runs on a side stream beside the CWS one
+  // (fork / join events on the caller's stream; graph-capture safe)
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 namespace {
@@ -498,6 +502,9 @@ int splitq_layer_destroy(splitq_layer_t L) {
   if (!L) return SPLITQ_OK;
   cudaSetDevice(L->device);
   for (cudaEvent_t e : L->ev_pool) cudaEventDestroy(e);
+  if (L->fork) cudaEventDestroy(L->fork);
+  if (L->join) cudaEventDestroy(L->join);
+  if (L->side) cudaStreamDestroy(L->side);
   L->mem.release();
   delete L;
   return SPLITQ_OK;
@@ -508,6 +515,9 @@ int splitq_layer_destroy(splitq_layer_t L) {
 static int64_t gv_scratch_bytes(const splitq_layer_s* L) {
   return 4 * (GV_MAX_ROWS * (L->r_s + L->r_c) + 4 * ((L->r_s + 15) / 16 + (L->r_c + 15) / 16));
 }
+
+// split-K scratch: the CWS first stage's slices first, the MAC stage's at this offset
+static int64_t lr1_scratch_off(const splitq_layer_s* L, int64_t T) { return round_up(8 * T * L->r_s * 4, 256); }
 
 int splitq_workspace_layout(splitq_layer_t L, int64_t T, splitq_ws_layout_t* o) {
   if (!L || !o) return fail(SPLITQ_ERR_INVALID, "null argument");
@@ -566,8 +576,9 @@ int splitq_workspace_layout(splitq_layer_t L, int64_t T, splitq_ws_layout_t* o) 
     const int64_t kmax = 8;  // split-K slices the scratch holds
     if (swap || m_tiles * ((L->d_out + bn - 1) / bn) * 2 <= pairs)
       need = std::max(need, kmax * T * L->d_out * 8);
-    for (int64_t r : {L->r_s, L->r_c})
-      if (r && (swap || m_tiles * 2 <= pairs)) need = std::max(need, kmax * T * r * 4);
+    // (the two LR1 launches may run concurrently: each has its own slices)
+    if ((L->r_s || L->r_c) && (swap || m_tiles * 2 <= pairs))
+      need = std::max(need, lr1_scratch_off(L, T) + kmax * T * L->r_c * 4);
     o->acc_scratch_bytes = need;
     o->acc_scratch = need ? take(need) : -1;
   }
@@ -1209,6 +1220,7 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   __half* lr_a = (__half*)at(W.lr_a);
 
   // ---- low-rank first stages: fp16 columns of the auxiliary operand
+  cudaStream_t lr_stream = stream;  // the LR1 launches' stream (the MAC one may fork)
   auto lr1 = [&](const void* a_codes, bool a_signed, const int8_t* bu, const float* su,
                  const int* csu, int64_t r, const float* row_s, const int* row_zp,
                  const int* m_count, const int* row_map, int64_t col_off, int64_t lo_off,
@@ -1251,7 +1263,11 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
               map_i8(&g.maps.b, bu, r, L->k_nat, L->ld_main, sw ? 128 : g.p.bn / 2);
     g.maps.xa = g.maps.xb = g.maps.a;
     if (!ok) return fail(SPLITQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (LR1)");
-    return launch_gemm(g, L->device, T, stream, at(W.acc_scratch), W.acc_scratch_bytes);
+    // the CWS and MAC stages may run concurrently: each its own split-K slices
+    const int64_t so = row_map ? lr1_scratch_off(L, T) : 0;
+    const int64_t sb = row_map ? W.acc_scratch_bytes - so : std::min(W.acc_scratch_bytes, lr1_scratch_off(L, T));
+    return launch_gemm(g, L->device, T, lr_stream, W.acc_scratch >= 0 && sb > 0 ? base + W.acc_scratch + so : nullptr,
+                       sb);
   };
   NvtxRange nv_lr1("splitq.LR1");
   if (gv && L->r_s && L->r_c) {  // decode: both first stages in one launch
@@ -1265,16 +1281,34 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
         (rc = launch_gv_pair(ps, L->act.centered, pc, L->aux.centered, (int)T, L->device, stream)))
       return rc;
   } else {
+  // both first stages: the MAC one forks onto the layer's side stream (the
+  // two are independent; with few tiles each they share the SMs)
+  const bool fork = L->r_s && L->r_c && !getenv("SPLITQ_LR1_SERIAL");
+  if (fork) {
+    if (!L->side) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&L->side, cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&L->fork, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&L->join, cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaEventRecord(L->fork, stream));
+    CUDA_TRY(cudaStreamWaitEvent(L->side, L->fork, 0));
+  }
   if (L->r_s &&
       (rc = lr1(at(W.a_main), L->act.centered, L->b_us, L->s_us, L->cs_us, L->r_s,
                 (const float*)at(W.lrs_main), L->act.centered ? nullptr : (const int*)at(W.zp_main),
                 nullptr, nullptr, L->off_s, L->r_s8)))
     return rc;
+  if (fork) lr_stream = L->side;
   if (L->r_c &&
       (rc = lr1(at(W.a_mac), L->aux.centered, L->b_uc, L->s_uc, L->cs_uc, L->r_c,
                 (const float*)at(W.lrs_mac), L->aux.centered ? nullptr : (const int*)at(W.zp_mac),
                 n_text, text_rows, L->off_c, 0)))
     return rc;
+  if (fork) {
+    lr_stream = stream;
+    CUDA_TRY(cudaEventRecord(L->join, L->side));
+    CUDA_TRY(cudaStreamWaitEvent(stream, L->join, 0));
+  }
   }
   if (prof && (rc = prof_record(L, stream))) return rc;
 
