@@ -282,6 +282,29 @@ __device__ __forceinline__ void kw_frac(const float (&z)[8], const uint32_t (&b)
   }
 }
 
+// f = v - n, compensated: z = x d as fl32(x d_hi) + (its exact error + x d_lo),
+// v = z (rs + rs_lo) with the exact error of the leading product, so
+// |f - (fl64(x d) / S - n)| <= 2^-23 + |v| 2^-40 (two fp32 roundings of
+// quantities below 0.52, then terms of relative size 2^-44)
+__device__ __forceinline__ void kw_frac_comp(const K1Params& p, int j, const float (&x)[8], const float (&d)[8],
+                                             const float (&z)[8], const uint32_t (&b)[8], const KwConsts& c,
+                                             float rs_lo, float (&f)[8]) {
+  const float4 la = __ldg(reinterpret_cast<const float4*>(p.d_main_lo32) + 2 * j);
+  const float4 lb = __ldg(reinterpret_cast<const float4*>(p.d_main_lo32) + 2 * j + 1);
+  const float dl[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const float plo = fmaf(x[e], d[e], -z[e]);   // x d_hi - fl32(x d_hi), exact
+    const float zl = fmaf(x[e], dl[e], plo);     // + x d_lo
+    const float vh = z[e] * c.rs;
+    float vl = fmaf(z[e], c.rs, -vh);            // exact error of vh
+    vl = fmaf(z[e], rs_lo, vl);
+    vl = fmaf(zl, c.rs, vl);
+    const float n = __uint_as_float(b[e] & ~c.fm) - c.base;
+    f[e] = (vh - n) + vl;
+  }
+}
+
 __device__ __forceinline__ uint32_t kw_minfrac(const uint32_t (&b)[8], uint32_t fm) {
   uint32_t m = b[0] & fm;
 #pragma unroll
@@ -796,6 +819,8 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
     }
     c = kw_shfl(c, 0);
     const double S = kw_shfl_d(gS, 0);
+    [[maybe_unused]] double rSm = 0.0;  // the main group's 1 / S (compensated MAC pass)
+    if constexpr (G64) rSm = kw_shfl_d(grS, 0);
     const int zp = __shfl_sync(0xffffffffu, gzp, 0);
     const RowParams rt = kw_rowparams(kw_shfl_d(gS, 1), kw_shfl_d(grS, 1),
                                       __shfl_sync(0xffffffffu, gzp, 1),
@@ -976,7 +1001,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
     double Se = 1.0;
     int zpe = 0;
     float ratio = 1.f;
-    int use_smf = 0;
+    int use_smf = 0, comp = 0;
     double rSe = 1.0;
     if (lane == 0) {
       if (!kw_params(elo64, ehi64, p.aux, &Se, &zpe, &rSe) && w0) atomicOr(p.err, ERR_SCALE_ZERO);
@@ -987,7 +1012,16 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
         ce = kw_consts2(elo64, ehi64, Se, rSe, zpe, p.aux, (ef + 1.52587890625e-05) * (S * rSe) * 1.01);
         use_smf = ce.safe && ce.W2 <= 16;
       }
-      if (!use_smf) ce = kw_consts2(elo64, ehi64, Se, rSe, zpe, p.aux, ef * (S * rSe) * 1.01);
+      if (G64 && !SMF && p.d_main_lo32 && S * rSe > 64.0) {
+        // wide aux codes: pass G forms f compensated (kw_frac_comp), |err| <=
+        // 2^-23 + vmax 2^-40 in units of S, so the fp32 code pass keeps a
+        // narrow window where the plain f would flag most chunks
+        ce = kw_consts2(elo64, ehi64, Se, rSe, zpe, p.aux,
+                        (1.1920928955078125e-07 + (double)vmaxf * 9.094947017729282e-13) * (S * rSe) * 1.01);
+        comp = 1;
+      } else if (!use_smf) {
+        ce = kw_consts2(elo64, ehi64, Se, rSe, zpe, p.aux, ef * (S * rSe) * 1.01);
+      }
       if (w0) {
         p.s_mac[slot] = Se;
         p.zp_mac[slot] = zpe;
@@ -1001,11 +1035,13 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
     zpe = __shfl_sync(0xffffffffu, zpe, 0);
     ratio = __shfl_sync(0xffffffffu, ratio, 0);
     use_smf = __shfl_sync(0xffffffffu, use_smf, 0);
+    comp = __shfl_sync(0xffffffffu, comp, 0);
 
     KW_STAMP(12)
     // ------------------------------------------------ pass G: MAC residual codes
     int8_t* erow = p.a_mac + (int64_t)slot * p.ld_main;
     qn = qnE;  // the chunks flagged in pass E are exact-coded here as well
+    [[maybe_unused]] const float rs_lo = G64 ? (float)(rSm - (double)c.rs) : 0.f;  // 1 / S = rs + rs_lo
     // fp64 pass G: when S / S_e is large (8-bit aux codes: ~255) the fp32
     // residual f = v - n carries too few bits for the MAC code (measured: 14 %
     // of chunks flagged, queue overflow on nearly every 18944-wide row). The
@@ -1015,7 +1051,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
     // fractions within 2^-30 of one half are flagged for the exact division.
     // (a separate instantiation, chosen on the host for wide aux codes: its
     // registers would cost the 4-bit configurations occupancy)
-    const bool g64 = G64 && !SMF && !allx && (!ce.safe || ratio > 64.f);
+    const bool g64 = G64 && !SMF && !allx && (!ce.safe || (ratio > 64.f && !comp));
     const bool allg = allx || (!ce.safe && !g64);
     if (g64) {
       for (int j0 = 0; j0 < nchunks; j0 += GT) {
@@ -1085,7 +1121,8 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
             else kwl(j, x, d);
             kw_mulz(x, d, z);
             kw_vt(z, c, b);
-            kw_frac(z, b, c, f);
+            if (G64 && comp) kw_frac_comp(p, j, x, d, z, b, c, rs_lo, f);
+            else kw_frac(z, b, c, f);
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
               const float2 t = kw_fma2(make_float2(f[2 * h], f[2 * h + 1]), make_float2(ratio, ratio),

@@ -163,6 +163,7 @@ struct K1Params {
   const int* c_main;
   const double* d_main;
   const float* d_main32;  // fp32 copy of d_main (K1 v3)
+  const float* d_main_lo32;  // fl32(d_main - d_main32) (K1w compensated MAC pass; may be null)
   const uint8_t* tags;    // modality tags (K1 v3 validates them)
   int n_main;
   int ld_main;  // row stride (bytes) of the main / MAC code matrices

@@ -182,6 +182,7 @@ struct splitq_layer_s {
   int64_t kt16 = 0, kv16 = 0, off_t = 0, off_v = 0, off_s = 0, off_c = 0, r_s8 = 0;
   DevBuf mem;
   int* c_main = nullptr; double* d_main = nullptr; float* d_main32 = nullptr;
+  float* d_main_lo32 = nullptr;  // fl32(d_main - d_main32): the compensated MAC pass (K1, wide aux codes)
   int k3_ok = 0;  // smoothing scales within the fp32 fast path's range
   int* c_text = nullptr; double* d_text = nullptr;
   int* c_vis = nullptr; double* d_vis = nullptr;
@@ -349,12 +350,16 @@ int splitq_layer_create(const splitq_layer_desc_t* d, int device, splitq_layer_t
     for (int64_t c = 0; c < L->d_in; ++c) cm[c] = (int32_t)c;
     std::vector<double> dm((size_t)L->ld_main, std::nan(""));
     for (int64_t k = 0; k < d->n_main; ++k) dm[d->c_main[k]] = d->scale_main[k];
-    std::vector<float> dm32((size_t)L->ld_main, std::nanf(""));
-    for (int64_t c = 0; c < L->ld_main; ++c) dm32[c] = (float)dm[c];
+    std::vector<float> dm32((size_t)L->ld_main, std::nanf("")), dmlo((size_t)L->ld_main, 0.f);
+    for (int64_t c = 0; c < L->ld_main; ++c) {
+      dm32[c] = (float)dm[c];
+      if (dm[c] == dm[c]) dmlo[c] = (float)(dm[c] - (double)dm32[c]);
+    }
     L->k3_ok = 1;
     for (int64_t k = 0; k < d->n_main; ++k)
       if (!(d->scale_main[k] > 1e-30 && d->scale_main[k] < 1e30)) L->k3_ok = 0;
     if ((rc = L->mem.upload(&L->d_main32, dm32.data(), dm32.size()))) return cleanup(rc);
+    if ((rc = L->mem.upload(&L->d_main_lo32, dmlo.data(), dmlo.size()))) return cleanup(rc);
     if ((rc = L->mem.upload(&L->c_main, cm.data(), cm.size()))) return cleanup(rc);
     if ((rc = L->mem.upload(&L->c_text, ct.data(), ct.size()))) return cleanup(rc);
     if ((rc = L->mem.upload(&L->c_vis, cv.data(), cv.size()))) return cleanup(rc);
@@ -1148,6 +1153,7 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   k.c_main = L->c_main;
   k.d_main = L->d_main;
   k.d_main32 = L->k3_ok ? L->d_main32 : nullptr;
+  k.d_main_lo32 = L->k3_ok && !getenv("SPLITQ_K1_NO_COMP") ? L->d_main_lo32 : nullptr;
   k.tags = tags;
   k.n_main = (int)L->k_nat;
   k.ld_main = (int)L->ld_main;

@@ -121,3 +121,52 @@ def test_bf16_sampled_rows_match_oracle():
     main = acc["main"] if gl.layout(T).code_centered_main else \
         acc["main"] + act["main"][2][:, None] * w["main"][0].sum(axis=0)[None, :]
     np.testing.assert_array_equal(raw[0][ridx].cpu().numpy().astype(np.int64), main)
+
+
+@pytest.mark.parametrize("name", ["q", "down"])
+def test_w4a8_sampled_rows_codes_bit_exact(name):
+    """W4A8 at the full step size: the 8-bit aux (MAC) codes take the
+    compensated fp32 residual pass (k1w.cuh kw_frac_comp) with its narrow
+    tie window. Sampled text rows of the full-size run: main and MAC codes,
+    scales and zero points bit-exact against the oracle on those rows."""
+    import bench
+    import paper_2605_19929_b200 as pkg
+    from paper_2605_19929_b200 import runtime
+    dev = torch.device("cuda", 0)
+    tags, inputs, layers = bench.build_workload(pkg, T, 8, 4)
+    g, sp, layer = next(t for t in layers if t[1].name == name)
+    x = bench.make_input_tensor(torch, dev, T, inputs[g], tags, 78)
+    gl = runtime.GpuLayer(layer, dev)
+    ws = gl.workspace(T)
+    gl.run(x, torch.from_numpy(tags).to(dev), ws=ws)
+    torch.cuda.synchronize()
+    lay = gl.layout(T)
+    wsn = ws.cpu().numpy()
+
+    def view(off, dt, n):
+        return wsn[off: off + np.dtype(dt).itemsize * n].view(dt)
+
+    text = np.flatnonzero(tags == 0)
+    rows = np.sort(np.random.default_rng(4).choice(text, 64, replace=False))
+    xs = x[torch.from_numpy(rows).to(dev)].double().cpu().numpy()
+    L = orc.from_reference_layer(layer)
+    act = orc.activation_codes(L, xs, tags[rows])
+    cm = np.asarray(layer.partition.c_main)
+    # main codes of the sampled rows
+    q, s, z = act["main"]
+    zp = view(lay.zp_main, np.int32, T).astype(np.int64)[rows]
+    np.testing.assert_array_equal(zp, z)
+    np.testing.assert_array_equal(view(lay.s_main, np.float64, T)[rows], s)
+    c = view(lay.a_main, np.int8, T * lay.ld_main).reshape(T, lay.ld_main)[rows][:, cm].astype(np.int64)
+    np.testing.assert_array_equal(c + zp[:, None] if lay.code_centered_main else (c & 0xFF), q)
+    # MAC codes: compact slots -> rows
+    q, s, z = act["mac"]
+    n_text = int(view(lay.n_text, np.int32, 1)[0])
+    slot_rows = view(lay.text_rows, np.int32, n_text)
+    slot_of = {int(r): i for i, r in enumerate(slot_rows)}
+    slots = np.array([slot_of[int(r)] for r in rows])
+    zpe = view(lay.zp_mac, np.int32, n_text).astype(np.int64)[slots]
+    np.testing.assert_array_equal(zpe, z)
+    np.testing.assert_array_equal(view(lay.s_mac, np.float64, n_text)[slots], s)
+    c = view(lay.a_mac, np.int8, n_text * lay.ld_main).reshape(n_text, lay.ld_main)[slots][:, cm].astype(np.int64)
+    np.testing.assert_array_equal(c + zpe[:, None] if lay.code_centered_aux else (c & 0xFF), q)
