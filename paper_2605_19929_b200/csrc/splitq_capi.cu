@@ -1119,6 +1119,18 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   if (!raw && (y_dtype != SPLITQ_F32 && y_dtype != SPLITQ_F16 && y_dtype != SPLITQ_BF16))
     return fail(SPLITQ_ERR_INVALID, "bad y dtype");
   if (y_ld < L->d_out) return fail(SPLITQ_ERR_INVALID, "y leading dimension too small");
+  // the layer's device is current for the call (its side stream, the
+  // launches); the caller's is restored on return
+  struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int d) {
+      if (cudaGetDevice(&prev) == cudaSuccess && prev != d) cudaSetDevice(d);
+      else prev = -1;
+    }
+    ~DeviceScope() {
+      if (prev >= 0) cudaSetDevice(prev);
+    }
+  } device_scope(L->device);
   splitq_ws_layout_t W;
   int rc = splitq_workspace_layout(L, T, &W);
   if (rc) return rc;
