@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -200,6 +201,7 @@ struct splitq_layer_s {
   // (fork / join events on the caller's stream; graph-capture safe)
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  std::mutex side_mu;  // creation + the fork / join enqueues (host threads may share a layer)
 };
 
 namespace {
@@ -1302,11 +1304,15 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
   // both first stages: the MAC one forks onto the layer's side stream (the
   // two are independent; with few tiles each they share the SMs)
   const bool fork = L->r_s && L->r_c && !getenv("SPLITQ_LR1_SERIAL");
+  // the fork ... join enqueue sequence holds the layer's lock: host threads
+  // sharing the layer must not interleave records of the shared events
+  std::unique_lock<std::mutex> side_lock(L->side_mu, std::defer_lock);
   if (fork) {
+    side_lock.lock();
     if (!L->side) {
-      CUDA_TRY(cudaStreamCreateWithFlags(&L->side, cudaStreamNonBlocking));
       CUDA_TRY(cudaEventCreateWithFlags(&L->fork, cudaEventDisableTiming));
       CUDA_TRY(cudaEventCreateWithFlags(&L->join, cudaEventDisableTiming));
+      CUDA_TRY(cudaStreamCreateWithFlags(&L->side, cudaStreamNonBlocking));
     }
     CUDA_TRY(cudaEventRecord(L->fork, stream));
     CUDA_TRY(cudaStreamWaitEvent(L->side, L->fork, 0));
@@ -1326,6 +1332,7 @@ int splitq_forward(splitq_layer_t L, const void* x, int x_dtype, int64_t x_ld, c
     lr_stream = stream;
     CUDA_TRY(cudaEventRecord(L->join, L->side));
     CUDA_TRY(cudaStreamWaitEvent(stream, L->join, 0));
+    side_lock.unlock();
   }
   }
   if (prof && (rc = prof_record(L, stream))) return rc;

@@ -194,7 +194,9 @@ class GpuLayer:
     def run(self, x, tags, y=None, out_dtype=None, raw=False, check=True, ws=None,
             profile=False, unpacked=False):
         """Launch the forward on the current stream. x: CUDA [T x >=d_in]
-        (f16/bf16/f32/f64, unit column stride), tags: CUDA uint8 [T]."""
+        (f16/bf16/f32/f64, unit column stride), tags: CUDA uint8 [T].
+        Without ws the layer's cached workspace is used: calls that may run
+        concurrently (other streams or threads) must each pass their own."""
         torch = _torch()
         lib = _lib.load()
         if not (_is_torch(x) and _is_torch(tags)):

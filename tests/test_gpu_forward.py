@@ -392,3 +392,40 @@ def test_fast_epilogue_bit_identical(name, dt, monkeypatch):
     monkeypatch.setenv("SPLITQ_EPI_SLOW", "1")
     b = g.run(xd, td, out_dtype=getattr(torch, dt)).cpu().numpy()
     np.testing.assert_array_equal(a, b)
+
+
+def test_concurrent_calls_share_a_layer():
+    """Host threads calling one layer on their own streams, each with its own
+    workspace (GpuLayer.run's cached workspace is per layer; the prefill
+    LR1 fork / join uses per-layer events and a side stream): every call's
+    output equals the serial one."""
+    import threading
+    from paper_2605_19929_b200 import runtime
+    layer, x, tags = _case(**CASES["c1_small"])
+    g = runtime.packed(layer)
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    td = torch.from_numpy(tags).cuda()
+    ref = g.run(xd, td).cpu().numpy()
+    outs, errs = [None] * 4, []
+
+    def work(i):
+        try:
+            s = torch.cuda.Stream()
+            ws = torch.empty(int(g.layout(x.shape[0]).total_bytes), dtype=torch.uint8, device="cuda")
+            torch.cuda.synchronize()
+            with torch.cuda.stream(s):
+                ys = [g.run(xd, td, ws=ws) for _ in range(8)]
+            s.synchronize()
+            outs[i] = [y.cpu().numpy() for y in ys]
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for o in outs:
+        for y in o:
+            np.testing.assert_array_equal(y, ref)
