@@ -292,16 +292,21 @@ __device__ __forceinline__ void kw_frac_comp(const K1Params& p, int j, const flo
   const float4 la = __ldg(reinterpret_cast<const float4*>(p.d_main_lo32) + 2 * j);
   const float4 lb = __ldg(reinterpret_cast<const float4*>(p.d_main_lo32) + 2 * j + 1);
   const float dl[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+  const float2 rs2 = make_float2(c.rs, c.rs), rl2 = make_float2(rs_lo, rs_lo);
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const float plo = fmaf(x[e], d[e], -z[e]);   // x d_hi - fl32(x d_hi), exact
-    const float zl = fmaf(x[e], dl[e], plo);     // + x d_lo
-    const float vh = z[e] * c.rs;
-    float vl = fmaf(z[e], c.rs, -vh);            // exact error of vh
-    vl = fmaf(z[e], rs_lo, vl);
-    vl = fmaf(zl, c.rs, vl);
-    const float n = __uint_as_float(b[e] & ~c.fm) - c.base;
-    f[e] = (vh - n) + vl;
+  for (int h = 0; h < 4; ++h) {  // two elements per packed op (each lane rounds as the scalar op)
+    const float2 x2 = make_float2(x[2 * h], x[2 * h + 1]), z2 = make_float2(z[2 * h], z[2 * h + 1]);
+    const float2 plo = kw_fma2(x2, make_float2(d[2 * h], d[2 * h + 1]), make_float2(-z2.x, -z2.y));  // exact
+    const float2 zl = kw_fma2(x2, make_float2(dl[2 * h], dl[2 * h + 1]), plo);                     // + x d_lo
+    const float2 vh = kw_mul2(z2, rs2);
+    float2 vl = kw_fma2(z2, rs2, make_float2(-vh.x, -vh.y));  // exact error of vh
+    vl = kw_fma2(z2, rl2, vl);
+    vl = kw_fma2(zl, rs2, vl);
+    const float2 n2 = kw_add2(make_float2(__uint_as_float(b[2 * h] & ~c.fm), __uint_as_float(b[2 * h + 1] & ~c.fm)),
+                              make_float2(-c.base, -c.base));
+    const float2 ff = kw_add2(kw_add2(vh, make_float2(-n2.x, -n2.y)), vl);
+    f[2 * h] = ff.x;
+    f[2 * h + 1] = ff.y;
   }
 }
 
