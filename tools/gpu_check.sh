@@ -1,5 +1,6 @@
-set -x
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?
-timeout 900 python -m pytest tests/test_gpu_k1v3.py -x -q > gpurun_out/pytest_k1v3.log 2>&1; echo k1v3 rc=$?
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
-timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e > gpurun_out/bench.log 2>&1; echo bench rc=$?
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu_r02b.log 2>&1; echo pytest rc=$?
+tail -3 gpurun_out/pytest_gpu_r02b.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()"; echo smoke rc=$?
+timeout 900 python bench.py > gpurun_out/bench_r02b.log 2> gpurun_out/bench_r02b.err; echo bench rc=$?
+cat gpurun_out/bench_r02b.log | head -c 1500
