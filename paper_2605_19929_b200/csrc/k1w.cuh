@@ -565,7 +565,8 @@ struct KwZ {
 // ahead. For few rows per warp on wide rows, where a warp's serial passes
 // are the critical path; it costs registers (occupancy) at full load.
 template <typename T, bool SMF, int WPR, bool SYNC = false, bool G64 = false, bool PF = false>
-__global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : KW_THREADS)
+__global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : KW_THREADS,
+                                  WPR > 1 ? 1 : SYNC ? 2 : 8)  // warp rows: 64 registers, 32 warps per SM
     k1w_kernel(const K1Params p, int d_in) {
   static_assert(!(SMF && WPR > 1), "SMEM MAC fractions are per-warp rows");
   extern __shared__ __align__(16) uint8_t kw_smem[];
@@ -617,8 +618,15 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
   // at d_in = 3584: 0.695 -> 0.61 ms; at 18944 rows vary more and the
   // barrier costs more than it saves (3.31 -> 4.6 ms), so it is not used.
   const int rstep = WPR > 1 ? (int)gridDim.x : nw;
-  for (int rb = WPR > 1 ? (int)blockIdx.x : (int)(blockIdx.x * nwc); rb < p.T; rb += rstep) {
+  // the tag of the storing lane's next row, loaded a row ahead (its value
+  // decides the MAC slot claim at the row's start)
+  const int rb0 = WPR > 1 ? (int)blockIdx.x : (int)(blockIdx.x * nwc);
+  uint8_t tg_next = 1;
+  if (lane == 0 && w0 && p.tags && rb0 + (WPR > 1 ? 0 : wl) < p.T) tg_next = p.tags[rb0 + (WPR > 1 ? 0 : wl)];
+  for (int rb = rb0; rb < p.T; rb += rstep) {
     const int row = WPR > 1 ? rb : rb + wl;
+    const uint8_t tg_row = tg_next;
+    if (lane == 0 && w0 && p.tags && row + rstep < p.T) tg_next = p.tags[row + rstep];
     if constexpr (WPR > 1) __syncthreads();  // the previous row's SMEM reads are done
     if (row < p.T) do {
     KW_STAMP(0)
@@ -633,6 +641,20 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
       else kw_load<T>(p, xg, j, x, d);
     };
 
+    // the row's tag and MAC slot (an atomic with return: an L2 round trip)
+    // are requested before pass A, so their latency hides under it
+    int slot = -1;
+    if (lane == 0 && w0) {
+      const uint8_t tg = tg_row;
+      if (tg > 1) atomicOr(p.err, ERR_BAD_TAG);
+      if (p.use_mac && tg == 0) {
+        if (p.mac_count) {
+          slot = atomicAdd(p.mac_count, 1);  // consumed after pass A (in-order issue)
+        } else if (p.text_idx) {
+          slot = p.text_idx[row];
+        }
+      }
+    }
     // row groups: the outlier channel indices and scales of this thread are
     // fetched before pass A, so only the x gather follows it
     int pc_t = -1, pc_v = -1;
@@ -692,19 +714,7 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
     }
     KW_STAMP(1)
     float L = kw_warp_minf(elo.m1), H = kw_warp_minf(ehi.m1);  // H = -max
-    int slot = -1;
-    if (lane == 0 && w0) {
-      const uint8_t tg = p.tags ? p.tags[row] : (uint8_t)1;
-      if (tg > 1) atomicOr(p.err, ERR_BAD_TAG);
-      if (p.use_mac && tg == 0) {
-        if (p.mac_count) {
-          slot = atomicAdd(p.mac_count, 1);
-          p.mac_rows[slot] = row;
-        } else if (p.text_idx) {
-          slot = p.text_idx[row];
-        }
-      }
-    }
+    if (lane == 0 && w0 && slot >= 0 && p.mac_count) p.mac_rows[slot] = row;
     slot = __shfl_sync(0xffffffffu, slot, 0);
 
     // outlier paths: exact fp64 extremes (every warp of a group: few channels)
@@ -984,7 +994,16 @@ __global__ void __launch_bounds__(WPR > 1 ? WPR * 32 : SYNC ? KW_THREADS_SYNC : 
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           if (f[u] <= bfl || -f[u] <= bfh) {
-            const double e64 = kw_exact_e(p, dm, kw_x<T>(xr, 8 * j + u), 8 * j + u, r);
+            // off the tie window the fast path's n is the exact code (safe
+            // row: no clipping), so e = z - n S needs no division
+            const int ch = 8 * j + u;
+            double e64;
+            if ((b[u] & c.fm) > c.W2) {
+              const float n = __uint_as_float(b[u] & ~c.fm) - c.base;
+              e64 = __dsub_rn(__dmul_rn((double)kw_x<T>(xr, ch), dm[ch]), __dmul_rn((double)n, S));
+            } else {
+              e64 = kw_exact_e(p, dm, kw_x<T>(xr, ch), ch, r);
+            }
             if (f[u] <= bfl) elo64 = fmin(elo64, e64);
             if (-f[u] <= bfh) ehi64 = fmax(ehi64, e64);
           }
