@@ -291,9 +291,20 @@ template <int MODE>
 __device__ __forceinline__ bool ts_member(int v, const int8_t* asg, int j) {
   return MODE != 0 || asg[v] == j;
 }
+// A rank count's value fl64(v / nc) (mocd.py:111). With fast set, the host
+// has checked, for every v in [0, nc], that the division-free form
+// q = fl(v rnc), x = fma(fma(-q, nc, v), rnc, q) (rnc = fl(1 / nc)) equals
+// the IEEE quotient, so the per-token division goes away bit-identically.
+__device__ __forceinline__ double ts_x(int v, double nc, double rnc, bool fast) {
+  const double dv = (double)v;
+  if (!fast) return dv / nc;
+  const double q = __dmul_rn(dv, rnc);
+  return __fma_rn(__fma_rn(-q, nc, dv), rnc, q);
+}
 template <int MODE>
-__device__ __forceinline__ double ts_value(int v, double nc, const int8_t* asg, const double* cen) {
-  const double x = (double)v / nc;
+__device__ __forceinline__ double ts_value(int v, double nc, double rnc, bool fast, const int8_t* asg,
+                                           const double* cen) {
+  const double x = ts_x(v, nc, rnc, fast);
   if (MODE == 0 || MODE == 2) return x;
   const double d = x - (MODE == 1 ? cen[asg[v]] : cen[0]);
   return __dmul_rn(d, d);  // numpy squares first, then sums: no FMA contraction
@@ -323,11 +334,12 @@ struct TokReader {
 
 // Pairwise sum of the next m member values from the reader (numpy recursion).
 template <int MODE>
-__device__ double ts_subtree(TokReader& rd, int m, int j, double nc, const int8_t* asg, const double* cen) {
+__device__ double ts_subtree(TokReader& rd, int m, int j, double nc, double rnc, bool fast, const int8_t* asg,
+                            const double* cen) {
   auto next = [&]() -> double {
     int v = rd.next();
     while (!ts_member<MODE>(v, asg, j)) v = rd.next();
-    return ts_value<MODE>(v, nc, asg, cen);
+    return ts_value<MODE>(v, nc, rnc, fast, asg, cen);
   };
   auto leaf = [&](int len) -> double {
     double res = 0.0;
@@ -376,8 +388,8 @@ __device__ double ts_subtree(TokReader& rd, int m, int j, double nc, const int8_
 // Exact pairwise sums for clusters 0..nk-1 (MODE 0) or the single all-token
 // sequence (MODE 1-3, nk = 1): results in sh.tot[j] and sh.nj[j].
 template <int MODE>
-__device__ void ts_pairwise_pass(const uint16_t* col, int n, int nk, double nc, const int8_t* asg,
-                                 const double* cen, TsShared& sh, bool vec) {
+__device__ void ts_pairwise_pass(const uint16_t* col, int n, int nk, double nc, double rnc, bool fast,
+                                 const int8_t* asg, const double* cen, TsShared& sh, bool vec) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int S = ((n + TS_THREADS - 1) / TS_THREADS + 7) & ~7;  // segments of whole 16-byte vectors
   const int t0 = min(n, tid * S), t1 = min(n, t0 + S);
@@ -454,7 +466,7 @@ __device__ void ts_pairwise_pass(const uint16_t* col, int n, int nk, double nc, 
       }
       TokReader rd;
       rd.start(col, tok, vec);
-      v = ts_subtree<MODE>(rd, len, j, nc, asg, cen);
+      v = ts_subtree<MODE>(rd, len, j, nc, rnc, fast, asg, cen);
     }
     sh.val[tid] = v;
     __syncthreads();
@@ -490,7 +502,7 @@ __device__ void ts_pairwise_pass(const uint16_t* col, int n, int nk, double nc, 
 // One CTA per candidate channel c (c0 + blockIdx.x). counts_t: [n_cand x ld] uint16.
 __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
     const uint16_t* counts_t, int64_t ld, int n_cand, int n_text, int k_req, int max_iter, int c0,
-    int c1, double* scores) {
+    int c1, double* scores, double rnc, int fast_div) {
   // SMEM: a bitmask of the levels present, then one region used twice: the
   // (cumulative) level histogram while the centres are initialised, then the
   // level -> cluster map, the segment counts and the subtree sums. The peak
@@ -511,6 +523,7 @@ __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
   const bool vec = (reinterpret_cast<uintptr_t>(col) & 15) == 0;  // 16-byte token loads
   const int tid = threadIdx.x;
   const double nc = (double)n_cand;
+  const bool fast = fast_div != 0;
   if (tid == 0) {
     sh.seg = seg;
     sh.val = val;
@@ -550,10 +563,10 @@ __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
   if (k <= 1) {
     release_hist();
     // np.var(values): mean = sum / n, then mean((v - mean)^2) (pairwise sums)
-    ts_pairwise_pass<2>(col, n, 1, nc, asg, centers, sh, vec);
+    ts_pairwise_pass<2>(col, n, 1, nc, rnc, fast, asg, centers, sh, vec);
     if (tid == 0) centers[0] = sh.tot[0] / (double)n;
     __syncthreads();
-    ts_pairwise_pass<3>(col, n, 1, nc, asg, centers, sh, vec);
+    ts_pairwise_pass<3>(col, n, 1, nc, rnc, fast, asg, centers, sh, vec);
     if (tid == 0) scores[c] = sh.tot[0] / (double)n;
     return;
   }
@@ -566,7 +579,7 @@ __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
       if (hist[mid] > idx) hi = mid;
       else lo = mid + 1;
     }
-    return (double)lo / nc;
+    return ts_x(lo, nc, rnc, fast);
   };
   if (tid < k) {  // np.quantile(values, (2j - 1) / (2k)), method 'linear'
     const double q = (double)(2 * (tid + 1) - 1) / (double)(2 * k);
@@ -588,7 +601,7 @@ __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
   auto assign_levels = [&](const double* cen, bool track) {
     for (int v = tid; v <= n_cand; v += TS_THREADS) {
       if (!((present[v >> 5] >> (v & 31)) & 1u)) continue;
-      const double x = (double)v / nc;
+      const double x = ts_x(v, nc, rnc, fast);
       int best = 0;
       double bd = fabs(x - cen[0]);
       for (int j = 1; j < k; ++j) {
@@ -607,7 +620,7 @@ __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
   for (int it = 0; it < max_iter; ++it) {
     if (tid == 0) changed = 0;
     // members.mean() per cluster in token order (numpy pairwise), in parallel
-    ts_pairwise_pass<0>(col, n, k, nc, asg, centers, sh, vec);
+    ts_pairwise_pass<0>(col, n, k, nc, rnc, fast, asg, centers, sh, vec);
     if (tid < k) new_centers[tid] = sh.nj[tid] > 0 ? sh.tot[tid] / (double)sh.nj[tid] : centers[tid];
     __syncthreads();
     assign_levels(new_centers, true);
@@ -618,7 +631,7 @@ __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
     if (!ch) break;
   }
   // mean((values - centers[assign])^2)
-  ts_pairwise_pass<1>(col, n, 1, nc, asg, centers, sh, vec);
+  ts_pairwise_pass<1>(col, n, 1, nc, rnc, fast, asg, centers, sh, vec);
   if (tid == 0) scores[c] = sh.tot[0] / (double)n;
 #ifdef TS_TRACE
   if (tid == 0 && blockIdx.x == 0)
@@ -769,9 +782,17 @@ int splitq_mocd_text_score(const uint16_t* counts_t, int64_t ld, int64_t n_cand,
     if (dev >= 0 && dev < 64) attr[dev] = true;
   }
   if (smem > 200 * 1024) return mfail(SPLITQ_ERR_UNSUPPORTED, "too many candidate channels");
+  // the division-free rank values (ts_x) where they match the IEEE quotient
+  // for every level of this denominator (checked here, host fma = device fma)
+  const double nc = (double)n_cand, rnc = 1.0 / nc;
+  int fast = 1;
+  for (int64_t v = 0; v <= n_cand && fast; ++v) {
+    const double dv = (double)v, q = dv * rnc;
+    fast = std::fma(std::fma(-q, nc, dv), rnc, q) == dv / nc;
+  }
   mocd_text_score_kernel<<<(unsigned)(c1 - c0), TS_THREADS, smem,
                            reinterpret_cast<cudaStream_t>(stream_)>>>(
-      counts_t, ld, (int)n_cand, (int)n_text, k, max_iter, (int)c0, (int)c1, scores);
+      counts_t, ld, (int)n_cand, (int)n_text, k, max_iter, (int)c0, (int)c1, scores, rnc, fast);
   return cudaGetLastError() == cudaSuccess ? SPLITQ_OK : mfail(SPLITQ_ERR_CUDA, "text score launch failed");
 }
 
