@@ -22,6 +22,7 @@
 #include <cstdint>
 #include <type_traits>
 #include <algorithm>
+#include <mutex>
 #include <cub/block/block_radix_sort.cuh>
 #include <string>
 
@@ -278,6 +279,8 @@ static_assert((1 << TS_DEPTH) == TS_THREADS, "one subtree per thread");
 struct TsShared {
   int* seg;          // [TS_THREADS][TS_KMAX] member counts -> exclusive bases
   double* val;       // [TS_THREADS] subtree sums
+  uint16_t* cmp;     // this CTA's member slots: cluster j, segment t at cmp[j * cs + t * S]
+  int64_t cs;        // per-cluster region (elements): TS_THREADS * S, S <= cs / TS_THREADS
   int nj[TS_KMAX];
   double tot[TS_KMAX];
 };
@@ -332,13 +335,46 @@ struct TokReader {
   }
 };
 
-// Pairwise sum of the next m member values from the reader (numpy recursion).
-template <int MODE>
-__device__ double ts_subtree(TokReader& rd, int m, int j, double nc, double rnc, bool fast, const int8_t* asg,
+// Cluster j's members in token order from the compacted slots: segment s
+// holds its members contiguously at base + s * S (16-byte aligned), and the
+// scanned bases give each segment's count.
+struct GapReader {
+  const uint16_t* base;
+  const int* seg;  // exclusive bases, [TS_THREADS][TS_KMAX]
+  int j, m, S, s, i, cnt;
+  TokReader rd;
+  __device__ __forceinline__ int count(int t) const {
+    const int b = seg[t * TS_KMAX + j];
+    return (t + 1 < TS_THREADS ? seg[(t + 1) * TS_KMAX + j] : m) - b;
+  }
+  // member index st lies in segment t0 (the last whose base <= st)
+  __device__ void start(const uint16_t* b, const int* sg, int jj, int mm, int SS, int t0, int st) {
+    base = b, seg = sg, j = jj, m = mm, S = SS, s = t0;
+    i = st - seg[t0 * TS_KMAX + j];
+    cnt = count(s);
+    rd.start(base + (int64_t)s * S, i, true);
+  }
+  __device__ __forceinline__ int next() {
+    while (i == cnt) {
+      ++s;
+      i = 0;
+      cnt = count(s);
+      rd.start(base + (int64_t)s * S, 0, true);
+    }
+    ++i;
+    return rd.next();
+  }
+};
+
+// Pairwise sum of the next m member values from the reader (numpy recursion);
+// SKIP: the reader yields every token and non-members are skipped here.
+template <int MODE, bool SKIP, class R>
+__device__ double ts_subtree(R& rd, int m, int j, double nc, double rnc, bool fast, const int8_t* asg,
                             const double* cen) {
   auto next = [&]() -> double {
     int v = rd.next();
-    while (!ts_member<MODE>(v, asg, j)) v = rd.next();
+    if (SKIP)
+      while (!ts_member<MODE>(v, asg, j)) v = rd.next();
     return ts_value<MODE>(v, nc, rnc, fast, asg, cen);
   };
   auto leaf = [&](int len) -> double {
@@ -395,19 +431,26 @@ __device__ void ts_pairwise_pass(const uint16_t* col, int n, int nk, double nc, 
   const int t0 = min(n, tid * S), t1 = min(n, t0 + S);
   TS_T0()
   if (MODE == 0) {
-    // per-segment member counts, scanned per cluster over the segments
-    int cnt[TS_KMAX];
-#pragma unroll
-    for (int j = 0; j < TS_KMAX; ++j) cnt[j] = 0;
+    // one read of the segment: each member's value goes to its cluster's
+    // slot for this segment, in token order (16-bit counters packed in two
+    // words: no indexed local array); the counts are then scanned per
+    // cluster over the segments
+    uint64_t c_lo = 0, c_hi = 0;
+    uint16_t* my = sh.cmp + (int64_t)tid * S;
     TokReader rd;
     rd.start(col, t0, vec);
     for (int i = t0; i < t1; ++i) {
-      const int a = asg[rd.next()];
-#pragma unroll
-      for (int j = 0; j < TS_KMAX; ++j) cnt[j] += a == j;
+      const int v = rd.next();
+      const int a = asg[v];
+      const int sh16 = 16 * (a & 3);
+      const int idx = (int)(((a < 4 ? c_lo : c_hi) >> sh16) & 0xFFFFu);
+      my[a * sh.cs + idx] = (uint16_t)v;
+      if (a < 4) c_lo += 1ull << sh16;
+      else c_hi += 1ull << sh16;
     }
 #pragma unroll
-    for (int j = 0; j < TS_KMAX; ++j) sh.seg[tid * TS_KMAX + j] = cnt[j];
+    for (int j = 0; j < TS_KMAX; ++j)
+      sh.seg[tid * TS_KMAX + j] = (int)(((j < 4 ? c_lo : c_hi) >> (16 * (j & 3))) & 0xFFFFu);
     __syncthreads();
     if (warp < nk) {  // warp j: exclusive scan of cluster j's counts
       const int j = warp;
@@ -448,25 +491,21 @@ __device__ void ts_pairwise_pass(const uint16_t* col, int n, int nk, double nc, 
     }
     double v = 0.0;
     if (own) {
-      // first member: token st (MODE != 0), else through the segment bases
-      int tok = st;
-      if (MODE == 0) {
-        int lo = 0, hi = TS_THREADS - 1;  // last segment whose base <= st
+      if (MODE == 0) {  // member st through the segment bases, then the compacted slots
+        int lo = 0, hi = TS_THREADS - 1;  // last segment whose base <= st and with members
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
           if (sh.seg[mid * TS_KMAX + j] <= st) lo = mid;
           else hi = mid - 1;
         }
-        int seen = sh.seg[lo * TS_KMAX + j];
+        GapReader gr;
+        gr.start(sh.cmp + (int64_t)j * sh.cs, sh.seg, j, m, S, lo, st);
+        v = ts_subtree<MODE, false>(gr, len, j, nc, rnc, fast, asg, cen);
+      } else {
         TokReader rd;
-        rd.start(col, min(n, lo * S), vec);
-        while (seen < st)
-          if (ts_member<MODE>(rd.next(), asg, j)) ++seen;
-        tok = rd.pos;
+        rd.start(col, st, vec);
+        v = ts_subtree<MODE, true>(rd, len, j, nc, rnc, fast, asg, cen);
       }
-      TokReader rd;
-      rd.start(col, tok, vec);
-      v = ts_subtree<MODE>(rd, len, j, nc, rnc, fast, asg, cen);
     }
     sh.val[tid] = v;
     __syncthreads();
@@ -502,7 +541,7 @@ __device__ void ts_pairwise_pass(const uint16_t* col, int n, int nk, double nc, 
 // One CTA per candidate channel c (c0 + blockIdx.x). counts_t: [n_cand x ld] uint16.
 __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
     const uint16_t* counts_t, int64_t ld, int n_cand, int n_text, int k_req, int max_iter, int c0,
-    int c1, double* scores, double rnc, int fast_div) {
+    int c1, double* scores, double rnc, int fast_div, uint16_t* scratch, int64_t scratch_cta) {
   // SMEM: a bitmask of the levels present, then one region used twice: the
   // (cumulative) level histogram while the centres are initialised, then the
   // level -> cluster map, the segment counts and the subtree sums. The peak
@@ -517,8 +556,10 @@ __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
   __shared__ TsShared sh;
   __shared__ double centers[TS_KMAX], new_centers[TS_KMAX];
   __shared__ int distinct, changed;
-  const int c = c0 + blockIdx.x;
-  if (c >= c1) return;
+  // persistent CTAs (each owns one scratch slot of compacted member values)
+  // take the channels c0 + blockIdx.x, + gridDim.x, ...
+  for (int c = c0 + (int)blockIdx.x; c < c1; c += (int)gridDim.x) {
+  __syncthreads();  // the previous channel's SMEM reads are done
   const uint16_t* col = counts_t + (int64_t)c * ld;
   const bool vec = (reinterpret_cast<uintptr_t>(col) & 15) == 0;  // 16-byte token loads
   const int tid = threadIdx.x;
@@ -527,6 +568,8 @@ __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
   if (tid == 0) {
     sh.seg = seg;
     sh.val = val;
+    sh.cmp = scratch + (int64_t)blockIdx.x * scratch_cta;
+    sh.cs = (int64_t)TS_THREADS * ((((n_text + TS_THREADS - 1) / TS_THREADS) + 7) & ~7);
   }
 
   for (int v = tid; v <= n_cand; v += TS_THREADS) hist[v] = 0;
@@ -568,7 +611,7 @@ __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
     __syncthreads();
     ts_pairwise_pass<3>(col, n, 1, nc, rnc, fast, asg, centers, sh, vec);
     if (tid == 0) scores[c] = sh.tot[0] / (double)n;
-    return;
+    continue;
   }
 
   // order statistic: value of the idx-th element of the sorted values
@@ -633,10 +676,11 @@ __global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
   // mean((values - centers[assign])^2)
   ts_pairwise_pass<1>(col, n, 1, nc, rnc, fast, asg, centers, sh, vec);
   if (tid == 0) scores[c] = sh.tot[0] / (double)n;
+  }  // channels
 #ifdef TS_TRACE
-  if (tid == 0 && blockIdx.x == 0)
-    printf("TS_TRACE n=%d k=%d passes=%llu count+scan=%llu subtrees=%llu fold=%llu\n", n, k,
-           ts_trace[4], ts_trace[0], ts_trace[1], ts_trace[2]);
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    printf("TS_TRACE passes=%llu count+scan=%llu subtrees=%llu fold=%llu\n", ts_trace[4], ts_trace[0],
+           ts_trace[1], ts_trace[2]);
 #endif
 }
 
@@ -760,6 +804,35 @@ int splitq_mocd_transpose_u16(const uint16_t* in, int64_t rows, int64_t cols, ui
   return cudaGetLastError() == cudaSuccess ? SPLITQ_OK : mfail(SPLITQ_ERR_CUDA, "transpose launch failed");
 }
 
+}  // extern "C"
+
+// The text score's per-device scratch (compacted member values), grown on
+// demand; the stream-ordered launches that use it are serialised per device
+// by the caller's stream, and a larger request frees the old buffer only
+// after the device has drained it.
+static uint16_t* ts_scratch(int dev, size_t bytes) {
+  static std::mutex mu;
+  static uint16_t* buf[64] = {};
+  static size_t cap[64] = {};
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cap[dev] < bytes) {
+    if (buf[dev]) {
+      cudaDeviceSynchronize();
+      cudaFree(buf[dev]);
+      buf[dev] = nullptr;
+      cap[dev] = 0;
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    buf[dev] = static_cast<uint16_t*>(p);
+    cap[dev] = bytes;
+  }
+  return buf[dev];
+}
+
+extern "C" {
+
 int splitq_mocd_text_score(const uint16_t* counts_t, int64_t ld, int64_t n_cand, int64_t n_text,
                            int k, int max_iter, int64_t c0, int64_t c1, double* scores,
                            void* stream_) {
@@ -790,9 +863,22 @@ int splitq_mocd_text_score(const uint16_t* counts_t, int64_t ld, int64_t n_cand,
     const double dv = (double)v, q = dv * rnc;
     fast = std::fma(std::fma(-q, nc, dv), rnc, q) == dv / nc;
   }
-  mocd_text_score_kernel<<<(unsigned)(c1 - c0), TS_THREADS, smem,
-                           reinterpret_cast<cudaStream_t>(stream_)>>>(
-      counts_t, ld, (int)n_cand, (int)n_text, k, max_iter, (int)c0, (int)c1, scores, rnc, fast);
+  // persistent grid: the resident CTAs, each with a scratch slot for the
+  // compacted member values of its channel (k regions of TS_THREADS
+  // segments), kept per device and grown on demand
+  int per_sm = 0, sms = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mocd_text_score_kernel, TS_THREADS, smem) !=
+          cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || per_sm < 1)
+    return mfail(SPLITQ_ERR_CUDA, "text score occupancy");
+  const int64_t grid = std::min<int64_t>(c1 - c0, (int64_t)per_sm * sms);
+  const int64_t seg = (((n_text + TS_THREADS - 1) / TS_THREADS) + 7) & ~7;
+  const int64_t per_cta = (int64_t)k * TS_THREADS * seg;
+  uint16_t* scratch = ts_scratch(dev, (size_t)(grid * per_cta) * sizeof(uint16_t));
+  if (!scratch) return mfail(SPLITQ_ERR_CUDA, "text score scratch allocation");
+  mocd_text_score_kernel<<<(unsigned)grid, TS_THREADS, smem, reinterpret_cast<cudaStream_t>(stream_)>>>(
+      counts_t, ld, (int)n_cand, (int)n_text, k, max_iter, (int)c0, (int)c1, scores, rnc, fast, scratch,
+      per_cta);
   return cudaGetLastError() == cudaSuccess ? SPLITQ_OK : mfail(SPLITQ_ERR_CUDA, "text score launch failed");
 }
 
