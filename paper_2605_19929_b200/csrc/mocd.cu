@@ -437,16 +437,43 @@ __device__ void ts_pairwise_pass(const uint16_t* col, int n, int nk, double nc, 
     // cluster over the segments
     uint64_t c_lo = 0, c_hi = 0;
     uint16_t* my = sh.cmp + (int64_t)tid * S;
-    TokReader rd;
-    rd.start(col, t0, vec);
-    for (int i = t0; i < t1; ++i) {
-      const int v = rd.next();
+    auto put = [&](int v) {
       const int a = asg[v];
       const int sh16 = 16 * (a & 3);
       const int idx = (int)(((a < 4 ? c_lo : c_hi) >> sh16) & 0xFFFFu);
       my[a * sh.cs + idx] = (uint16_t)v;
       if (a < 4) c_lo += 1ull << sh16;
       else c_hi += 1ull << sh16;
+    };
+    if (vec) {  // t0 is a multiple of 8: whole 16-byte vectors, 8 tokens each
+      const uint4* c4 = reinterpret_cast<const uint4*>(col);
+      for (int p = t0; p < t1; p += 8) {
+        const uint4 w = __ldg(c4 + (p >> 3));
+        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+        if (p + 8 <= t1) {
+          // the 8 level -> cluster lookups first (independent), then the
+          // counter chain and the stores
+          int vv[8], aa[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) vv[u] = (int)((ww[u >> 1] >> (16 * (u & 1))) & 0xFFFFu);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) aa[u] = asg[vv[u]];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int a = aa[u], sh16 = 16 * (a & 3);
+            const int idx = (int)(((a < 4 ? c_lo : c_hi) >> sh16) & 0xFFFFu);
+            my[a * sh.cs + idx] = (uint16_t)vv[u];
+            if (a < 4) c_lo += 1ull << sh16;
+            else c_hi += 1ull << sh16;
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (p + u < t1) put((int)((ww[u >> 1] >> (16 * (u & 1))) & 0xFFFFu));
+        }
+      }
+    } else {
+      for (int i = t0; i < t1; ++i) put(col[i]);
     }
 #pragma unroll
     for (int j = 0; j < TS_KMAX; ++j)
@@ -539,7 +566,7 @@ __device__ void ts_pairwise_pass(const uint16_t* col, int n, int nk, double nc, 
 }
 
 // One CTA per candidate channel c (c0 + blockIdx.x). counts_t: [n_cand x ld] uint16.
-__global__ void __launch_bounds__(TS_THREADS) mocd_text_score_kernel(
+__global__ void __launch_bounds__(TS_THREADS, 2) mocd_text_score_kernel(
     const uint16_t* counts_t, int64_t ld, int n_cand, int n_text, int k_req, int max_iter, int c0,
     int c1, double* scores, double rnc, int fast_div, uint16_t* scratch, int64_t scratch_cta) {
   // SMEM: a bitmask of the levels present, then one region used twice: the
