@@ -834,15 +834,14 @@ int splitq_mocd_transpose_u16(const uint16_t* in, int64_t rows, int64_t cols, ui
 }  // extern "C"
 
 // The text score's per-device scratch (compacted member values), grown on
-// demand; the stream-ordered launches that use it are serialised per device
-// by the caller's stream, and a larger request frees the old buffer only
-// after the device has drained it.
+// demand. The caller holds ts_mu from the request through the launch, so a
+// larger request (which drains the device before freeing the old buffer)
+// cannot free a buffer whose kernel has not been enqueued yet.
+static std::mutex ts_mu;
 static uint16_t* ts_scratch(int dev, size_t bytes) {
-  static std::mutex mu;
   static uint16_t* buf[64] = {};
   static size_t cap[64] = {};
   if (dev < 0 || dev >= 64) return nullptr;
-  std::lock_guard<std::mutex> lk(mu);
   if (cap[dev] < bytes) {
     if (buf[dev]) {
       cudaDeviceSynchronize();
@@ -901,6 +900,7 @@ int splitq_mocd_text_score(const uint16_t* counts_t, int64_t ld, int64_t n_cand,
   const int64_t grid = std::min<int64_t>(c1 - c0, (int64_t)per_sm * sms);
   const int64_t seg = (((n_text + TS_THREADS - 1) / TS_THREADS) + 7) & ~7;
   const int64_t per_cta = (int64_t)k * TS_THREADS * seg;
+  std::lock_guard<std::mutex> lk(ts_mu);
   uint16_t* scratch = ts_scratch(dev, (size_t)(grid * per_cta) * sizeof(uint16_t));
   if (!scratch) return mfail(SPLITQ_ERR_CUDA, "text score scratch allocation");
   mocd_text_score_kernel<<<(unsigned)grid, TS_THREADS, smem, reinterpret_cast<cudaStream_t>(stream_)>>>(
