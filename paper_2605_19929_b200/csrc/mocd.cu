@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 #include <algorithm>
 #include <mutex>
@@ -223,6 +224,94 @@ int launch_rc_items(const void* x, int64_t ld, const int* rows, const int* n_tex
   if (need <= 48) return launch_rc<T, 48>(x, ld, rows, n_text, max_text, cand, n_cand, counts, s);
   if (need <= 80) return launch_rc<T, 80>(x, ld, rows, n_text, max_text, cand, n_cand, counts, s);
   return mfail(SPLITQ_ERR_UNSUPPORTED, "at most 20480 candidate channels");
+}
+
+// 16-bit inputs (fp16 / bf16): |x| is the bit pattern with the sign cleared,
+// and those 15-bit keys order like the values, so a row's counts come from a
+// histogram over all 32768 keys (two 16-bit bins per word, 64 KB of SMEM),
+// its inclusive prefix sum, and one lookup per candidate: the count of keys
+// <= the candidate's own key (searchsorted side='right', mocd.py:109-110).
+// No sort and no binary search per element.
+constexpr int RC16_THREADS = 512;
+constexpr int RC16_WORDS = 16384;  // 32768 bins
+size_t rc16_smem_bytes() { return (size_t)RC16_WORDS * 4 + 64 * 4; }
+
+__global__ void __launch_bounds__(RC16_THREADS) mocd_rank_counts16_kernel(
+    const void* x, int64_t ld, const int* text_rows, const int* n_text, const int* cand, int n_cand,
+    uint16_t* counts) {
+  extern __shared__ __align__(16) uint32_t rc16_smem[];
+  uint32_t* h = rc16_smem;                   // [RC16_WORDS]: bins 2w (low half), 2w + 1 (high half)
+  uint32_t* wsum = rc16_smem + RC16_WORDS;   // [RC16_THREADS / 32]
+  const int i = blockIdx.x;
+  if (i >= *n_text) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint16_t* xr = reinterpret_cast<const uint16_t*>(x) + (int64_t)text_rows[i] * ld;
+  for (int w = tid; w < RC16_WORDS; w += RC16_THREADS) h[w] = 0u;
+  __syncthreads();
+  for (int j = tid; j < n_cand; j += RC16_THREADS) {
+    const uint32_t k = (uint32_t)__ldg(xr + __ldg(cand + j)) & 0x7FFFu;
+    atomicAdd(h + (k >> 1), 1u << (16 * (k & 1)));
+  }
+  __syncthreads();
+  // inclusive prefix over the 32768 bins: thread t owns words [32 t, 32 t + 32)
+  constexpr int PER = RC16_WORDS / RC16_THREADS;
+  uint32_t* mine = h + tid * PER;
+  uint32_t tot = 0;
+#pragma unroll 8
+  for (int q = 0; q < PER; ++q) {
+    const uint32_t w = mine[q];
+    tot += (w & 0xFFFFu) + (w >> 16);
+  }
+  uint32_t inc = tot;  // block exclusive scan of the per-thread totals
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t v = lane < RC16_THREADS / 32 ? wsum[lane] : 0u, iv = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, iv, o);
+      if (lane >= o) iv += y;
+    }
+    if (lane < RC16_THREADS / 32) wsum[lane] = iv - v;
+  }
+  __syncthreads();
+  uint32_t run = wsum[warp] + inc - tot;  // keys in the bins before this thread's
+#pragma unroll 8
+  for (int q = 0; q < PER; ++q) {
+    const uint32_t w = mine[q];
+    const uint32_t lo = run + (w & 0xFFFFu), hi = lo + (w >> 16);
+    mine[q] = lo | (hi << 16);  // cumulative counts <= n_cand < 65536
+    run = hi;
+  }
+  __syncthreads();
+  uint16_t* out = counts + (int64_t)i * n_cand;
+  for (int j = tid; j < n_cand; j += RC16_THREADS) {
+    const uint32_t k = (uint32_t)__ldg(xr + __ldg(cand + j)) & 0x7FFFu;
+    out[j] = (uint16_t)((h[k >> 1] >> (16 * (k & 1))) & 0xFFFFu);
+  }
+}
+
+int launch_rc16(const void* x, int64_t ld, const int* rows, const int* n_text, int64_t max_text,
+                const int* cand, int n_cand, uint16_t* counts, cudaStream_t s) {
+  const size_t smem = rc16_smem_bytes();
+  static bool attr[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return mfail(SPLITQ_ERR_CUDA, "cudaGetDevice");
+  if (dev < 0 || dev >= 64 || !attr[dev]) {
+    if (cudaFuncSetAttribute(mocd_rank_counts16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return mfail(SPLITQ_ERR_CUDA, "cudaFuncSetAttribute (rank counts)");
+    if (dev >= 0 && dev < 64) attr[dev] = true;
+  }
+  mocd_rank_counts16_kernel<<<(unsigned)max_text, RC16_THREADS, smem, s>>>(x, ld, rows, n_text, cand,
+                                                                          n_cand, counts);
+  return cudaGetLastError() == cudaSuccess ? SPLITQ_OK
+                                           : mfail(SPLITQ_ERR_CUDA, "rank counts launch failed");
 }
 
 // ---------------------------------------------------------------- transpose
@@ -813,8 +902,13 @@ int splitq_mocd_rank_counts(const void* x, int x_dtype, int64_t x_ld, const int3
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream_);
   const int nc = (int)n_cand;
   switch (x_dtype) {
-    case SPLITQ_F16: return launch_rc_items<__half>(x, x_ld, text_rows, n_text, max_text, cand, nc, counts, s);
-    case SPLITQ_BF16: return launch_rc_items<__nv_bfloat16>(x, x_ld, text_rows, n_text, max_text, cand, nc, counts, s);
+    case SPLITQ_F16:  // 16-bit keys: histogram counts (SPLITQ_MOCD_RC_SORT=1: the sort path)
+    case SPLITQ_BF16:
+      if (!getenv("SPLITQ_MOCD_RC_SORT") && nc < 65536)
+        return launch_rc16(x, x_ld, text_rows, n_text, max_text, cand, nc, counts, s);
+      return x_dtype == SPLITQ_F16
+                 ? launch_rc_items<__half>(x, x_ld, text_rows, n_text, max_text, cand, nc, counts, s)
+                 : launch_rc_items<__nv_bfloat16>(x, x_ld, text_rows, n_text, max_text, cand, nc, counts, s);
     case SPLITQ_F32: return launch_rc_items<float>(x, x_ld, text_rows, n_text, max_text, cand, nc, counts, s);
     case SPLITQ_F64: return launch_rc_items<double>(x, x_ld, text_rows, n_text, max_text, cand, nc, counts, s);
     default: return mfail(SPLITQ_ERR_INVALID, "bad x dtype");

@@ -103,3 +103,21 @@ def test_stability_report_matches_reference():
     np.testing.assert_array_equal([r["mean_jaccard"] for r in rep], d["mean"])
     np.testing.assert_array_equal([r["std_jaccard"] for r in rep], d["std"])
     assert [r["subset_size"] for r in rep] == [int(s) for s in d["sizes"]]
+
+
+@pytest.mark.parametrize("n_cand_dim", [40, 3000])
+def test_rank_counts_bf16_histogram(n_cand_dim):
+    """bf16 rows take the 16-bit histogram rank counts (as fp16 rows do);
+    counts equal the oracle's on the exact values the bf16 rows hold."""
+    _, mg = _pkg()
+    rng = np.random.default_rng(11 + n_cand_dim)
+    n_text, n_vis = 300, 50
+    x = rng.standard_normal((n_text + n_vis, n_cand_dim)) * rng.uniform(0.05, 8, n_cand_dim)
+    x[:, ::5] = np.round(x[:, ::5])  # repeated keys (ties count via <=)
+    xt = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16)
+    xd = xt.float().numpy().astype(np.float64)
+    tags = rng.permutation(np.array([0] * n_text + [1] * n_vis, np.uint8))
+    cand = np.arange(n_cand_dim)[rng.random(n_cand_dim) > 0.1]
+    counts = mg._GPU.rank_counts(xt.cuda(), torch.from_numpy(tags).cuda(), cand)
+    np.testing.assert_array_equal(counts.cpu().numpy().astype(np.int64) & 0xFFFF,
+                                  mo.rank_counts(xd, tags, cand))
