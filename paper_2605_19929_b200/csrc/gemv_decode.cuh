@@ -132,7 +132,7 @@ __device__ __forceinline__ void gv_body(const GvMaps& maps, const G2Params& p, c
   const int um_per = (g.units_main + ks_n - 1) / ks_n;
   const int items = blocks * ks_n;
   auto unit_range = [&](int item, int& u0, int& u1) {
-    const int ks = item % ks_n;
+    const int ks = ks_n == 1 ? 0 : item % ks_n;
     u0 = ks * um_per;
     u1 = LR1 || ks_n > 1 ? min(g.units_main, u0 + um_per) : g.units_main + g.units_aux;
   };
@@ -149,22 +149,23 @@ __device__ __forceinline__ void gv_body(const GvMaps& maps, const G2Params& p, c
     if (lane == 0) {
       tma_prefetch(&maps.w);
       if (!LR1) tma_prefetch(&maps.x);
-      int li = 0;
+      int li = 0, st_i = 0;  // ring slot and fill round of unit li, kept incrementally
+      uint32_t round = 0;    // (no integer division / modulo by the runtime S per unit)
       for (int item = bid; item < items; item += nbid) {
         int u0, u1;
         unit_range(item, u0, u1);
-        const int cb = item / ks_n;
+        const int cb = ks_n == 1 ? item : item / ks_n;
         for (int u = u0; u < u1; ++u, ++li) {
           const bool aux = u >= g.units_main;
           const int b0 = (aux ? u - g.units_main : u) * GV_BPU;
           const int nb = min(GV_BPU, (aux ? g.nbox_aux : g.nbox) - b0);
-          const int st_i = li % S;
-          if (li >= S) mbar_wait(empty + st_i, (uint32_t)((li / S) - 1) & 1u);
+          if (li >= S) mbar_wait(empty + st_i, (round - 1u) & 1u);
           uint8_t* st = ring + st_i * GV_BPU * GV_BOX_BYTES;
           mbar_arrive_expect_tx(full + st_i, (uint32_t)(nb * GV_BOX_BYTES));
           for (int b = 0; b < nb; ++b)
             tma_load_2d(st + b * GV_BOX_BYTES, aux ? &maps.x : &maps.w, full + st_i,
                         aux ? (b0 + b) * 64 : (b0 + b) * 128, cb * 16);
+          if (++st_i == S) st_i = 0, ++round;
         }
       }
     }
@@ -234,9 +235,10 @@ __device__ __forceinline__ void gv_body(const GvMaps& maps, const G2Params& p, c
     arow[j] = sact + r * g.act_stride;
     xrow[j] = saux + r * g.aux_stride;
   }
-  int li = 0;
+  int li = 0, st_i = 0;
+  uint32_t round = 0;
   for (int item = bid; item < items; item += nbid) {
-    const int cb = item / ks_n;
+    const int cb = ks_n == 1 ? item : item / ks_n;
     int u0, u1;
     unit_range(item, u0, u1);
     // the block's column constants (channels cb*16 + gq and + 8), loaded now
@@ -264,9 +266,8 @@ __device__ __forceinline__ void gv_body(const GvMaps& maps, const G2Params& p, c
       const bool aux = u >= g.units_main;
       const int b0 = (aux ? u - g.units_main : u) * GV_BPU;
       const int nb = min(GV_BPU, (aux ? g.nbox_aux : g.nbox) - b0);
-      const int st_i = li % S;
       const uint8_t* st = ring + st_i * GV_BPU * GV_BOX_BYTES;
-      mbar_wait(full + st_i, (uint32_t)(li / S) & 1u);
+      mbar_wait(full + st_i, round & 1u);
       for (int it = warp; it < 2 * nb; it += GV_WARPS) {
         const int b = it >> 1, half = it & 1;
         const int c = 2 * tig + half;  // chunk of the 128-byte box row
@@ -311,6 +312,7 @@ __device__ __forceinline__ void gv_body(const GvMaps& maps, const G2Params& p, c
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + st_i);  // this warp is done with the stage
+      if (++st_i == S) st_i = 0, ++round;
     }
     // ---- per n-tile: the 8 warps' partials, summed in warp order by warp 0
 #pragma unroll
