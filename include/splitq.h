@@ -182,7 +182,9 @@ int splitq_mocd_absmax(const void* x, int x_dtype, int64_t x_ld, const uint8_t* 
 /* percentile_rank numerators (mocd.py:92-111): counts[i][j] =
  * #{l in cand : |x[r_i, l]| <= |x[r_i, cand[j]]|} for the text rows
  * r_i = text_rows[i], i < *n_text (device count, max_text rows allocated);
- * uint16 [max_text x n_cand], row-major. */
+ * uint16 [max_text x n_cand], row-major. fp16 / bf16 rows: a 32K-key
+ * histogram per row (SPLITQ_MOCD_RC_SORT=1 selects the sort path used for
+ * fp32 / fp64 rows). */
 int splitq_mocd_rank_counts(const void* x, int x_dtype, int64_t x_ld, const int32_t* text_rows,
                             const int32_t* n_text, int64_t max_text, const int32_t* cand,
                             int64_t n_cand, uint16_t* counts, void* stream);
@@ -194,7 +196,13 @@ int splitq_mocd_transpose_u16(const uint16_t* in, int64_t rows, int64_t cols, ui
  * evaluated with numpy's exact float64 arithmetic (quantile init,
  * pairwise-sum means). counts_t: uint16 [>= c1 x ld] (transposed counts of
  * a channel range); n_cand: the rank denominator |C'| (the counts lie in
- * 1..n_cand); scores fp64, scores[c] written for c in [c0, c1). */
+ * 1..n_cand); scores fp64, scores[c] written for c in [c0, c1). Rows that
+ * start 16-byte aligned are read in whole 16-byte vectors: the buffer must
+ * extend to the next multiple of 8 tokens past each such row (ld a multiple
+ * of 8, as mocd_gpu allocates it).
+ * The library keeps one device scratch buffer per device for the compacted
+ * cluster members (k x 512 x ceil8(n_text / 512) uint16 per resident CTA),
+ * grown on demand under a lock held through the launch. */
 int splitq_mocd_text_score(const uint16_t* counts_t, int64_t ld, int64_t n_cand, int64_t n_text,
                            int k, int max_iter, int64_t c0, int64_t c1, double* scores,
                            void* stream);
