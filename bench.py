@@ -92,12 +92,12 @@ _UNIT_BYTES = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e1
 
 def ncu_gemm_traffic(path=None):
     """DRAM bytes per split-GEMM launch (dram__bytes_read.sum + write.sum) from
-    the committed `ncu --set full` capture of one bench step (profiles/r02b,
+    the committed `ncu --set full` capture of one bench step (profiles/r02c,
     tools/gpu_profile.sh): the mean over the captured SPLIT-mode launches
     (every third launch of the kernel: LR1 CWS, LR1 MAC, split). None if
     absent. ncu's raw page reports these in Gbyte."""
-    path = path or os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02b",
-                                "ncu_gemm_r02b.json")
+    path = path or os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02c",
+                                "ncu_gemm_r02c.json")
     try:
         ks = json.load(open(path))["kernels"]
     except (OSError, ValueError, KeyError):
