@@ -369,6 +369,7 @@ struct TsShared {
   int* seg;          // [TS_THREADS][TS_KMAX] member counts -> exclusive bases
   double* val;       // [TS_THREADS] subtree sums
   uint16_t* cmp;     // this CTA's member slots: cluster j, segment t at cmp[j * cs + t * S]
+  uint16_t* sbuf;    // SMEM store buffers: 8 members per (cluster, thread), written out 16 B at a time
   int64_t cs;        // per-cluster region (elements): TS_THREADS * S, S <= cs / TS_THREADS
   int nj[TS_KMAX];
   double tot[TS_KMAX];
@@ -526,11 +527,21 @@ __device__ void ts_pairwise_pass(const uint16_t* col, int n, int nk, double nc, 
     // cluster over the segments
     uint64_t c_lo = 0, c_hi = 0;
     uint16_t* my = sh.cmp + (int64_t)tid * S;
+    // members collect 8 at a time in this thread's SMEM buffer of their
+    // cluster and leave as one 16-byte store (2-byte stores scattered over
+    // 32 slots per warp instruction were the pass's bound)
+    uint16_t* sb = sh.sbuf + tid * 8;  // cluster a: sb + a * TS_THREADS * 8
+    auto emit = [&](int a, int idx, int v) {
+      uint16_t* b = sb + a * (TS_THREADS * 8);
+      b[idx & 7] = (uint16_t)v;
+      if ((idx & 7) == 7)
+        *reinterpret_cast<uint4*>(my + a * sh.cs + (idx & ~7)) = *reinterpret_cast<const uint4*>(b);
+    };
     auto put = [&](int v) {
       const int a = asg[v];
       const int sh16 = 16 * (a & 3);
       const int idx = (int)(((a < 4 ? c_lo : c_hi) >> sh16) & 0xFFFFu);
-      my[a * sh.cs + idx] = (uint16_t)v;
+      emit(a, idx, v);
       if (a < 4) c_lo += 1ull << sh16;
       else c_hi += 1ull << sh16;
     };
@@ -551,7 +562,7 @@ __device__ void ts_pairwise_pass(const uint16_t* col, int n, int nk, double nc, 
           for (int u = 0; u < 8; ++u) {
             const int a = aa[u], sh16 = 16 * (a & 3);
             const int idx = (int)(((a < 4 ? c_lo : c_hi) >> sh16) & 0xFFFFu);
-            my[a * sh.cs + idx] = (uint16_t)vv[u];
+            emit(a, idx, vv[u]);
             if (a < 4) c_lo += 1ull << sh16;
             else c_hi += 1ull << sh16;
           }
@@ -563,6 +574,11 @@ __device__ void ts_pairwise_pass(const uint16_t* col, int n, int nk, double nc, 
       }
     } else {
       for (int i = t0; i < t1; ++i) put(col[i]);
+    }
+    for (int j = 0; j < nk; ++j) {  // the partial buffers (< 8 members each)
+      const int cnt = (int)(((j < 4 ? c_lo : c_hi) >> (16 * (j & 3))) & 0xFFFFu);
+      const uint16_t* b = sb + j * (TS_THREADS * 8);
+      for (int q = cnt & ~7; q < cnt; ++q) my[j * sh.cs + q] = b[q & 7];
     }
 #pragma unroll
     for (int j = 0; j < TS_KMAX; ++j)
@@ -669,6 +685,8 @@ __global__ void __launch_bounds__(TS_THREADS, 2) mocd_text_score_kernel(
   double* val = reinterpret_cast<double*>(region);                         // [TS_THREADS]        (after)
   int* seg = reinterpret_cast<int*>(val + TS_THREADS);                     // [TS_THREADS x KMAX] (after)
   int8_t* asg = reinterpret_cast<int8_t*>(seg + TS_THREADS * TS_KMAX);     // [n_cand + 1]        (after)
+  uint16_t* sbuf = reinterpret_cast<uint16_t*>(
+      (reinterpret_cast<uintptr_t>(asg + n_cand + 1) + 15) & ~uintptr_t(15));  // [k][TS_THREADS][8] (after)
   __shared__ TsShared sh;
   __shared__ double centers[TS_KMAX], new_centers[TS_KMAX];
   __shared__ int distinct, changed;
@@ -685,6 +703,7 @@ __global__ void __launch_bounds__(TS_THREADS, 2) mocd_text_score_kernel(
     sh.seg = seg;
     sh.val = val;
     sh.cmp = scratch + (int64_t)blockIdx.x * scratch_cta;
+    sh.sbuf = sbuf;
     sh.cs = (int64_t)TS_THREADS * ((((n_text + TS_THREADS - 1) / TS_THREADS) + 7) & ~7);
   }
 
@@ -963,7 +982,8 @@ int splitq_mocd_text_score(const uint16_t* counts_t, int64_t ld, int64_t n_cand,
   if (k > TS_KMAX) return mfail(SPLITQ_ERR_UNSUPPORTED, "at most 8 clusters on the GPU path");
   if (c1 <= c0) return SPLITQ_OK;
   const size_t bits = (size_t)(((n_cand + 32) / 32 * 4 + 15) & ~15);
-  const size_t after = (size_t)TS_THREADS * 8 + (size_t)TS_THREADS * TS_KMAX * 4 + (size_t)(n_cand + 1);
+  const size_t after = (size_t)TS_THREADS * 8 + (size_t)TS_THREADS * TS_KMAX * 4 + (size_t)(n_cand + 1) + 16 +
+                       (size_t)k * TS_THREADS * 16;  // + the compaction store buffers
   const size_t smem = bits + std::max((size_t)(n_cand + 1) * 4, after) + 16;
   static bool attr[64] = {};  // per device (the attribute is per context)
   int dev = 0;
