@@ -444,15 +444,46 @@ struct GapReader {
     cnt = count(s);
     rd.start(base + (int64_t)s * S, i, true);
   }
+  bool stale = false;  // rd not positioned at i (after a next8)
   __device__ __forceinline__ int next() {
     while (i == cnt) {
       ++s;
       i = 0;
       cnt = count(s);
       rd.start(base + (int64_t)s * S, 0, true);
+      stale = false;
+    }
+    if (stale) {
+      rd.start(base + (int64_t)s * S, i, true);
+      stale = false;
     }
     ++i;
     return rd.next();
+  }
+  // the next 8 members at once when they lie in the current segment: two
+  // aligned 16-byte loads and a funnel shift by the offset (the scratch is
+  // padded past its end for the second load); false -> use next()
+  __device__ __forceinline__ bool next8(int (&v)[8]) {
+    if (i + 8 > cnt) return false;
+    const uint4* p4 = reinterpret_cast<const uint4*>(base + (int64_t)s * S) + (i >> 3);
+    const uint4 a = __ldg(p4), b = __ldg(p4 + 1);
+    const uint32_t x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const int k = (i & 7) >> 1, sh = 16 * (i & 1);
+    uint32_t y[5];  // y[q] = x[k + q]
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const uint32_t x0 = x[q], x1 = x[q + 1], x2 = x[q + 2], x3 = x[min(q + 3, 7)];
+      y[q] = k == 0 ? x0 : k == 1 ? x1 : k == 2 ? x2 : x3;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t w = __funnelshift_r(y[q], y[q + 1], sh);
+      v[2 * q] = (int)(w & 0xFFFFu);
+      v[2 * q + 1] = (int)(w >> 16);
+    }
+    i += 8;
+    stale = true;
+    return true;
   }
 };
 
@@ -474,12 +505,32 @@ __device__ double ts_subtree(R& rd, int m, int j, double nc, double rnc, bool fa
       return res;
     }
     double r[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) r[u] = next();
     const int body = len - len % 8;
-    for (int q = 8; q < body; q += 8) {
+    if constexpr (std::is_same<R, GapReader>::value) {  // compacted members: 8 at a time
+      int v8[8];
+      if (rd.next8(v8)) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) r[u] += next();
+        for (int u = 0; u < 8; ++u) r[u] = ts_value<MODE>(v8[u], nc, rnc, fast, asg, cen);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) r[u] = next();
+      }
+      for (int q = 8; q < body; q += 8) {
+        if (rd.next8(v8)) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) r[u] += ts_value<MODE>(v8[u], nc, rnc, fast, asg, cen);
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) r[u] += next();
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) r[u] = next();
+      for (int q = 8; q < body; q += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) r[u] += next();
+      }
     }
     res = ts_combine8(r);
     for (int q = body; q < len; ++q) res += next();
@@ -1015,7 +1066,7 @@ int splitq_mocd_text_score(const uint16_t* counts_t, int64_t ld, int64_t n_cand,
   const int64_t seg = (((n_text + TS_THREADS - 1) / TS_THREADS) + 7) & ~7;
   const int64_t per_cta = (int64_t)k * TS_THREADS * seg;
   std::lock_guard<std::mutex> lk(ts_mu);
-  uint16_t* scratch = ts_scratch(dev, (size_t)(grid * per_cta) * sizeof(uint16_t));
+  uint16_t* scratch = ts_scratch(dev, (size_t)(grid * per_cta + 16) * sizeof(uint16_t));  // + next8 read pad
   if (!scratch) return mfail(SPLITQ_ERR_CUDA, "text score scratch allocation");
   mocd_text_score_kernel<<<(unsigned)grid, TS_THREADS, smem, reinterpret_cast<cudaStream_t>(stream_)>>>(
       counts_t, ld, (int)n_cand, (int)n_text, k, max_iter, (int)c0, (int)c1, scores, rnc, fast, scratch,
