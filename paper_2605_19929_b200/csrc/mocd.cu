@@ -373,6 +373,7 @@ struct TsShared {
   int64_t cs;        // per-cluster region (elements): TS_THREADS * S, S <= cs / TS_THREADS
   int nj[TS_KMAX];
   double tot[TS_KMAX];
+  int dirty;  // MODE 0: bit j set -> cluster j's member set changed since its last sum
 };
 
 // Member test and value of token value v for pass `mode`:
@@ -658,6 +659,9 @@ __device__ void ts_pairwise_pass(const uint16_t* col, int n, int nk, double nc, 
   __syncthreads();
   TS_T(0)
   for (int j = 0; j < nk; ++j) {
+    // a cluster whose members did not change keeps its sum (and its mean):
+    // the same members in the same token order give the same pairwise sum
+    if (MODE == 0 && !((sh.dirty >> j) & 1)) continue;
     const int m = sh.nj[j];
     // this thread's subtree: the D bits of tid from the root
     int st = 0, len = m;
@@ -740,7 +744,7 @@ __global__ void __launch_bounds__(TS_THREADS, 2) mocd_text_score_kernel(
       (reinterpret_cast<uintptr_t>(asg + n_cand + 1) + 15) & ~uintptr_t(15));  // [k][TS_THREADS][8] (after)
   __shared__ TsShared sh;
   __shared__ double centers[TS_KMAX], new_centers[TS_KMAX];
-  __shared__ int distinct, changed;
+  __shared__ int distinct, changed, dirty_next;
   // persistent CTAs (each owns one scratch slot of compacted member values)
   // take the channels c0 + blockIdx.x, + gridDim.x, ...
   for (int c = c0 + (int)blockIdx.x; c < c1; c += (int)gridDim.x) {
@@ -840,22 +844,31 @@ __global__ void __launch_bounds__(TS_THREADS, 2) mocd_text_score_kernel(
           best = j;
         }
       }
-      if (track && asg[v] != (int8_t)best) changed = 1;
+      if (track && asg[v] != (int8_t)best) {
+        changed = 1;
+        atomicOr(&dirty_next, (1 << asg[v]) | (1 << best));
+      }
       asg[v] = (int8_t)best;
     }
   };
   assign_levels(centers, false);
   __syncthreads();
+  if (tid == 0) sh.dirty = (1 << k) - 1;  // the first means come from the quantile centres
   for (int it = 0; it < max_iter; ++it) {
-    if (tid == 0) changed = 0;
-    // members.mean() per cluster in token order (numpy pairwise), in parallel
+    if (tid == 0) changed = 0, dirty_next = 0;
+    // members.mean() per cluster in token order (numpy pairwise), in parallel;
+    // clusters whose members did not change keep their centre (the mean of
+    // the same members, computed last iteration)
     ts_pairwise_pass<0>(col, n, k, nc, rnc, fast, asg, centers, sh, vec);
-    if (tid < k) new_centers[tid] = sh.nj[tid] > 0 ? sh.tot[tid] / (double)sh.nj[tid] : centers[tid];
+    if (tid < k)
+      new_centers[tid] = !((sh.dirty >> tid) & 1) ? centers[tid]
+                         : sh.nj[tid] > 0 ? sh.tot[tid] / (double)sh.nj[tid] : centers[tid];
     __syncthreads();
     assign_levels(new_centers, true);
     if (tid < k) centers[tid] = new_centers[tid];
     __syncthreads();
     const int ch = changed;
+    if (tid == 0) sh.dirty = dirty_next;
     __syncthreads();  // every thread has read the flag before thread 0 resets it
     if (!ch) break;
   }
