@@ -121,3 +121,30 @@ def test_rank_counts_bf16_histogram(n_cand_dim):
     counts = mg._GPU.rank_counts(xt.cuda(), torch.from_numpy(tags).cuda(), cand)
     np.testing.assert_array_equal(counts.cpu().numpy().astype(np.int64) & 0xFFFF,
                                   mo.rank_counts(xd, tags, cand))
+
+
+@pytest.mark.parametrize("n_text,k", [(1001, 3), (77, 4), (3, 2)])
+def test_text_score_unpadded_rows(n_text, k):
+    """The C-ABI text score on a transposed count matrix whose row stride is
+    not a whole number of 16-byte vectors (rows alternate between the vector
+    and the scalar reader, and between the vectorised and the scalar
+    compaction): scores equal the oracle's k-means bit for bit. The buffer
+    extends one vector past the last row (the contract in splitq.h)."""
+    import ctypes as C
+    from paper_2605_19929_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(1000 + n_text)
+    n_cand, w = 300, 37
+    counts = rng.integers(1, n_cand + 1, (n_text, w))
+    counts[:, ::5] = rng.integers(1, 4, (n_text, len(range(0, w, 5))))  # few levels
+    ld = n_text  # no padding between rows
+    buf = np.zeros(w * ld + 16, np.int16)
+    buf[: w * ld] = counts.T.reshape(-1).astype(np.int16)
+    dev = torch.from_numpy(buf).cuda()
+    scores = torch.zeros(w, dtype=torch.float64, device="cuda")
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    _lib.check(lib.splitq_mocd_text_score(dev.data_ptr(), ld, n_cand, n_text, k, 50, 0, w,
+                                          scores.data_ptr(), st))
+    got = scores.cpu().numpy()
+    ref = np.array([mo.kmeans_1d_exact(counts[:, c], n_cand, min(k, n_text), 50) for c in range(w)])
+    np.testing.assert_array_equal(got, ref)
